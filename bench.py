@@ -1,0 +1,397 @@
+"""Benchmark of the B200 hot path: batched env reset/step (random_script +
+realize) fused with event labelling and mode classification, plus event
+list emission (and, for N>1, the NCCL label all-gather + mode-histogram
+all-reduce).
+
+Workload (BASELINE.json configs[1], "C2"): Place skill, 1024 parallel envs
+per GPU; each env runs one random-action rollout = fuzz(seed, Place,
+FuzzConfig(max_gap=64, max_tail=64)) (~200 env steps); every bench step
+uses fresh seeds.  Metric: env samples/sec (records generated + labelled
+per second, whole job), with labelled trajectories/sec alongside.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ENV = 1024
+KIND = 1  # Place
+CFG = dict(max_events=8, max_gap=64, max_tail=64, edge_density=1.0, success_prob=0.5)
+RECORD_BYTES = 93  # 23 f32 planes + 1 u8 grasped (dof 7), SURVEY 8(d)
+LABEL_BYTES = 24
+WORKLOAD = ("C2: Place, 1024 envs/GPU, random-action rollout per env = "
+            "fuzz(seed, Place, FuzzConfig(max_gap=64, max_tail=64)) (~200 steps), "
+            "fresh seeds every step; generation + events + modes (+ event lists)")
+METRIC = "env samples/sec (SPS)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for n, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profile_traffic():
+    """dram bytes/launch of k_synth from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get("k_synth_dram_bytes_per_launch"), d.get("k_synth_records_per_launch")
+    except Exception:
+        return None, None
+
+
+def cpu_baseline(seconds, n_threads=1):
+    """CPU oracle (C restatement of the reference path) on a bounded sample."""
+    from oracle import oracle as O
+    cfg = O.fuzz_cfg(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail", "edge_density",
+                                            "success_prob")})
+    n, recs, t = 64, 0, 0.0
+    seed = 10 ** 9
+    while t < seconds:
+        t0 = time.perf_counter()
+        r, *_ = O.fuzz_label_batch(seed, n, KIND, cfg, n_threads=n_threads, want_outputs=False)
+        t += time.perf_counter() - t0
+        recs += r
+        seed += n
+        n = min(n * 2, 1 << 16)
+    eps = seed - 10 ** 9
+    return recs / t, eps / t, f"{eps} episodes ({recs} env steps) of the bench workload, {t:.1f} s"
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference path's CPU implementation (the C
+    oracle port, all host threads) on the same workload."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    cfg = O.fuzz_cfg(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail", "edge_density",
+                                            "success_prob")})
+    n_env = N_ENV * world
+    for k in range(args.warmup):
+        O.fuzz_label_batch(-(k + 1) * n_env - 10 ** 8, n_env, KIND, cfg, n_threads=cores, want_outputs=False)
+    recs, t0 = 0, time.perf_counter()
+    for k in range(args.steps):
+        r, *_ = O.fuzz_label_batch(k * n_env, n_env, KIND, cfg, n_threads=cores, want_outputs=False)
+        recs += r
+    dt = time.perf_counter() - t0
+    sps = recs / dt
+    out = {"impl": "reference", "metric": METRIC, "value": sps, "unit": "env-steps/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "trajectories_per_sec": n_env * args.steps / dt,
+           "config": {"workload": WORKLOAD, "envs_per_step": n_env},
+           "cpu_baseline": {"value": sps, "unit": "env-steps/s", "cores": cores, "kind": "port",
+                            "sample": f"{args.steps} steps x {n_env} episodes, oracle/oracle.c "
+                                      "(C restatement of trajlab fuzz+extract_events+classify), "
+                                      f"{cores} threads"},
+           "e2e": {"value": sps, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import ctypes
+    import torch
+    from paper_2412_13211_b200 import _lib as L
+    from paper_2412_13211_b200 import core
+    from paper_2412_13211_b200.synth import FuzzConfig
+    from paper_2412_13211_b200.thresholds import Thresholds
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    lib = L.lib()
+    cfg = FuzzConfig(**CFG)
+    cap = core.fuzz_capacity(cfg)
+    ws = core.SynthWorkspace(N_ENV, cap)
+    cs = core.synth_csets(Thresholds()).to_device(dev)
+    th_c = core.thresholds_c(Thresholds())
+    cfg_c = L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0, cfg.edge_density,
+                        cfg.success_prob)
+    K, W = args.steps, args.warmup
+    # inputs resident in HBM: seeds of every step, rank-disjoint ranges
+    all_seeds = (torch.arange(K + W, device=dev, dtype=torch.int64)[:, None] * world + rank) * N_ENV \
+        + torch.arange(N_ENV, device=dev, dtype=torch.int64)[None, :]
+    seeds_buf = torch.empty(N_ENV, dtype=torch.int64, device=dev)
+    ev_cap = N_ENV * cap
+    ev_off = torch.empty(N_ENV + 1, dtype=torch.int64, device=dev)
+    ev_kind = torch.empty(ev_cap, dtype=torch.uint8, device=dev)
+    ev_t = torch.empty(ev_cap, dtype=torch.int32, device=dev)
+    scan_scratch = torch.empty(max(16, lib.tl_scan_scratch_bytes(N_ENV)), dtype=torch.uint8, device=dev)
+    hist = torch.zeros(L.N_MODES, dtype=torch.int64, device=dev)
+    gathered = torch.empty((world, N_ENV, 24), dtype=torch.uint8, device=dev) if world > 1 else None
+    rb = ws.records()
+    rb_c = rb.c()
+    stream = torch.cuda.current_stream()
+
+    def synth_only(s):
+        sp = ctypes.c_void_p(s.cuda_stream)
+        L.check(lib.tl_fuzz(L.ptr(seeds_buf), N_ENV, KIND, ctypes.byref(cfg_c), ctypes.byref(th_c),
+                            L.ptr(cs), None, ctypes.byref(rb_c), cap, None, None, None,
+                            L.ptr(ws.step_mask), L.ptr(ws.labels), sp), "tl_fuzz")
+
+    def step_body(s):
+        sp = ctypes.c_void_p(s.cuda_stream)
+        synth_only(s)
+        L.check(lib.tl_scan_events(L.ptr(ws.labels), N_ENV, L.ptr(ev_off), L.ptr(scan_scratch), sp),
+                "scan")
+        L.check(lib.tl_emit_events(L.ptr(ws.step_mask), L.ptr(ws.rec_start), L.ptr(ws.n_rec),
+                                   L.ptr(ws.labels), L.ptr(ev_off), N_ENV, L.ptr(ev_kind),
+                                   L.ptr(ev_t), sp), "emit")
+        if world > 1:
+            L.check(lib.tl_mode_histogram(L.ptr(ws.labels), N_ENV, L.ptr(hist), sp), "hist")
+
+    launches_per_step = 5 + (1 if world > 1 else 0)
+
+    # warm-up (also sets kernel attributes before graph capture)
+    seeds_buf.copy_(all_seeds[0])
+    step_body(stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step_body(torch.cuda.current_stream())
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def collectives():
+        if world > 1:
+            dist.all_gather_into_tensor(gathered.view(-1), ws.labels.view(-1))
+            dist.all_reduce(hist)
+
+    for k in range(W):
+        seeds_buf.copy_(all_seeds[K + k])
+        graph.replay()
+        collectives()
+    torch.cuda.synchronize()
+
+    # ---- device-timed steps: inputs in HBM, L2 flushed between steps -------
+    nrec_log = torch.empty((K, N_ENV), dtype=torch.int32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    gpu_id = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) if \
+        os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    with ClockSampler(gpu_id) as clocks:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            ev[k][0].record(stream)
+            seeds_buf.copy_(all_seeds[k])
+            graph.replay()
+            collectives()
+            ev[k][1].record(stream)
+            nrec_log[k].copy_(ws.n_rec)
+            flush.zero_()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+
+        # ---- k_synth alone (roofline of the dominant kernel) ---------------
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            seeds_buf.copy_(all_seeds[k])
+            kev[k][0].record(stream)
+            synth_only(stream)
+            kev[k][1].record(stream)
+            flush.zero_()
+        torch.cuda.synchronize()
+        synth_ms = [a.elapsed_time(b) for a, b in kev]
+
+        # ---- end to end: host seeds -> device -> host records + labels -----
+        host_seeds = all_seeds.cpu().pin_memory()
+        comp_planes = torch.empty((23, N_ENV * cap), dtype=torch.float32, device=dev)
+        comp_g = torch.empty(N_ENV * cap, dtype=torch.uint8, device=dev)
+        comp_start = torch.empty(N_ENV + 1, dtype=torch.int64, device=dev)
+        comp_nrec = torch.empty(N_ENV, dtype=torch.int32, device=dev)
+        comp_c = L.Records_c(comp_planes.data_ptr(), comp_g.data_ptr(), comp_start.data_ptr(),
+                             comp_nrec.data_ptr(), N_ENV * cap, 0, 7)
+        h_planes = torch.empty((23, N_ENV * cap), dtype=torch.float32).pin_memory()
+        h_g = torch.empty(N_ENV * cap, dtype=torch.uint8).pin_memory()
+        h_labels = torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory()
+        h_evoff = torch.empty(N_ENV + 1, dtype=torch.int64).pin_memory()
+        h_evk = torch.empty(ev_cap, dtype=torch.uint8).pin_memory()
+        h_evt = torch.empty(ev_cap, dtype=torch.int32).pin_memory()
+        K2 = max(1, min(K, 50))
+        e2e_ms, h2d_b, d2h_b, e2e_recs = [], 0, 0, 0
+        for k in range(K2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            seeds_buf.copy_(host_seeds[k], non_blocking=True)
+            graph.replay()
+            collectives()
+            sp = ctypes.c_void_p(stream.cuda_stream)
+            L.check(lib.tl_scan_counts(L.ptr(ws.n_rec), N_ENV, L.ptr(comp_start), L.ptr(scan_scratch), sp), "scan")
+            L.check(lib.tl_compact_records(ctypes.byref(rb_c), N_ENV, L.ptr(comp_start),
+                                           ctypes.byref(comp_c), sp), "compact")
+            # result sizes (one 16-byte read), then exactly the produced bytes
+            tot = torch.stack([comp_start[N_ENV], ev_off[N_ENV]]).cpu()
+            R, NE = int(tot[0]), int(tot[1])
+            for p in range(23):
+                h_planes[p, :R].copy_(comp_planes[p, :R], non_blocking=True)
+            h_g[:R].copy_(comp_g[:R], non_blocking=True)
+            h_labels.copy_(ws.labels, non_blocking=True)
+            h_evoff.copy_(ev_off, non_blocking=True)
+            h_evk[:NE].copy_(ev_kind[:NE], non_blocking=True)
+            h_evt[:NE].copy_(ev_t[:NE], non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+            e2e_recs += R
+            h2d_b = N_ENV * 8
+            d2h_b = R * RECORD_BYTES + N_ENV * 24 + (N_ENV + 1) * 8 + NE * 5 + 16
+            flush.zero_()
+    clk = clocks.summary()
+
+    recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
+    total_recs = float(recs_per_step.sum().item())
+    t_dev = sum(step_ms) / 1e3
+    t_syn = sum(synth_ms) / 1e3
+    t_e2e = sum(e2e_ms) / 1e3
+    tt = torch.tensor([t_dev, t_syn, t_e2e, total_recs, float(e2e_recs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = tt[:3].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt[3:].clone()
+        dist.all_reduce(sm)
+        t_dev, t_syn, t_e2e = mx.tolist()
+        total_recs, e2e_recs_all = sm.tolist()
+    else:
+        e2e_recs_all = float(e2e_recs)
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    hbm_peak, peak_src = peaks()
+    recs_per_launch = total_recs / world / K
+    alg_bytes = recs_per_launch * RECORD_BYTES + N_ENV * LABEL_BYTES
+    achieved = alg_bytes / (t_syn / K) / 1e9
+    traffic_b, traffic_recs = profile_traffic()
+    traffic = None
+    if traffic_b and traffic_recs:
+        traffic = traffic_b / traffic_recs * recs_per_launch
+    cb_sps, cb_eps, cb_sample = cpu_baseline(args.cpu_seconds)
+    sps = total_recs / t_dev
+    out = {
+        "metric": METRIC, "value": sps, "unit": "env-steps/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * t_dev / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "storage": "f32 records",
+        "data": "synthetic",
+        "trajectories_per_sec": N_ENV * world * K / t_dev,
+        "config": {"workload": WORKLOAD, "envs_per_gpu": N_ENV, "subtask": "Place",
+                   "fuzz_config": CFG, "mean_steps_per_episode": recs_per_launch / N_ENV,
+                   "parallelism": f"episodes sharded over {world} GPU(s), NCCL label all-gather",
+                   "l2": "flushed between timed steps (256 MiB write, excluded from timing)",
+                   "timing": "CUDA events per step on the launch stream, max over ranks",
+                   "step": "1 CUDA graph: tl_fuzz + tl_scan_events + tl_emit_events"
+                           + (" + tl_mode_histogram, then NCCL all_gather/all_reduce" if world > 1 else "")},
+        "gpu_launches": launches_per_step * K,
+        "roofline": {"kernel": "k_synth (tl_fuzz)", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": 1e3 * t_syn / K,
+                     "note": "93 B/record + 24 B/episode written; MT19937 + f64 generation is "
+                             "ALU/latency-bound, not HBM-bound (SURVEY 8(d))"},
+        "e2e": {"value": e2e_recs_all / t_e2e, "unit": "env-steps/s",
+                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
+                "steps": K2, "note": "pinned host seeds -> GPU -> compact records, labels "
+                                      "and event lists back to pinned host memory"},
+        "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
+                         "sample": cb_sample, "trajectories_per_sec": cb_eps},
+        "clocks": clk,
+    }
+    print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

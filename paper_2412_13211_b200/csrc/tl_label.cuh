@@ -1,0 +1,757 @@
+// tl_label.cuh -- predicates, edge-triggered events and mode classification.
+//
+// Reference (paths under /root/reference/pkg/src/trajlab/):
+//   predicates.py:16-99   j_max / is_static / _at_rest / success_step
+//   events.py:94-193      extract_events (edge tests in EVENT_ORDER)
+//   modes.py:24-253       last_index / _Ctx / rule tables / classify
+//
+// Mapping: one warp per episode, lane = timestep within a 32-record chunk.
+// Each lane evaluates its record's indicator bits; the previous record's
+// bits arrive by __shfl_up (carry across chunks); events are the per-step
+// bitmask in EVENT_ORDER bit order.  The event list itself is never stored
+// here: classification needs only |E|, the last index of each kind and d0
+// (modes.py:42-61), kept as warp-uniform registers (ballot + clz + scan).
+//
+// Numerics: the reference compares binary32 record values widened to f64
+// against f64 thresholds.  For f32 records every such compare is done
+// exactly in f32 against a directed-rounding cut (tl_cset, host-built):
+//   x <= T <=> x <= rd(T),  x > T <=> x > rd(T),  x >= T <=> x >= ru(T),
+//   x < T <=> x < ru(T).
+// Differences against a nonzero rest posture (j_max, torso) are f64.
+// f64 records (arbitrary doubles, e.g. text logs) use f64 compares.
+#pragma once
+#include "tl_common.cuh"
+
+namespace tl {
+
+// ---- comparison overloads: f32 value vs cut, f64 value vs threshold -------
+__device__ __forceinline__ bool LE(float x, float c, double) { return x <= c; }
+__device__ __forceinline__ bool LE(double x, float, double t) { return x <= t; }
+__device__ __forceinline__ bool GT(float x, float c, double) { return x > c; }
+__device__ __forceinline__ bool GT(double x, float, double t) { return x > t; }
+__device__ __forceinline__ bool GE(float x, float c, double) { return x >= c; }
+__device__ __forceinline__ bool GE(double x, float, double t) { return x >= t; }
+__device__ __forceinline__ bool LT(float x, float c, double) { return x < c; }
+__device__ __forceinline__ bool LT(double x, float, double t) { return x < t; }
+__device__ __forceinline__ float tabs(float x) { return fabsf(x); }
+__device__ __forceinline__ double tabs(double x) { return fabs(x); }
+
+// indicator bits of one record
+enum : uint32_t {
+  IND_CONTACT = 1u, IND_GRASPED = 2u, IND_SUCCESS = 4u, IND_CUM_LE = 8u,
+  IND_CUM_GT = 16u, IND_A = 32u, IND_B = 64u
+};
+// per-record error bits
+enum : uint32_t { ERR_SUCC = 1u, ERR_FORCE = 2u, ERR_DIST = 4u, ERR_ART = 8u };
+
+// Python max() over a generator of |v_i| (a leading NaN sticks, later NaNs
+// never win): m = v0; m = v if v > m.
+template <class T>
+__device__ __forceinline__ T pymax_step(T m, T v) { return v > m ? v : m; }
+
+// Record values the predicates need (lane-private).
+template <class T>
+struct RecV {
+  T der, dist, force, cum, art, tor, vx, vy, om, qdm;
+  T jm;          // Python-max |q_i - rest_i| when rest is zero (T path)
+  double jm_d;   // same, f64, for a nonzero rest posture
+  bool g;
+};
+
+// _at_rest (predicates.py:64-72)
+template <class T>
+__device__ __forceinline__ bool at_rest(const tl_cset& c, const RecV<T>& v, bool torso) {
+  if (GT(v.der, c.rd_rest_radius, c.rest_radius)) return false;
+  const bool jm_over = c.rest_zero ? GT(v.jm, c.rd_j_arm, c.j_arm) : (v.jm_d > c.j_arm);
+  if (jm_over) return false;
+  if (torso) {
+    const bool tor_over = c.rest_zero
+                              ? GT(tabs(v.tor), c.rd_j_tor, c.j_tor)
+                              : (fabs(__dsub_rn((double)v.tor, c.rest_tor)) > c.j_tor);
+    if (tor_over) return false;
+  }
+  // is_static (predicates.py:23-27)
+  return LE(v.qdm, c.rd_static_qd, c.static_qd) &&
+         LE(tabs(v.vx), c.rd_static_v, c.static_v) &&
+         LE(tabs(v.vy), c.rd_static_v, c.static_v) &&
+         LE(tabs(v.om), c.rd_static_om, c.static_om);
+}
+
+// success_step (predicates.py:75-94) + the per-record indicator bits used by
+// extract_events (events.py:103-190).  sc_* is the Close slightly-closed cut
+// anchored at records[0].art_q (events.py:174-176).
+template <class T>
+__device__ __forceinline__ void record_bits(const tl_cset& c, const RecV<T>& v,
+                                            float sc_ru, double sc_d,
+                                            uint32_t& ind, uint32_t& err) {
+  const bool over = GT(v.cum, c.rd_limit, c.limit);
+  ind = (LE(v.cum, c.rd_limit, c.limit) ? IND_CUM_LE : 0u) | (over ? IND_CUM_GT : 0u);
+  err = 0u;
+  bool succ = false;
+  switch (c.subtask) {
+    case TL_PICK:
+      succ = !over && v.g && at_rest(c, v, false);
+      ind |= (GT(v.force, c.rd_contact, c.contact_eps) ? IND_CONTACT : 0u) |
+             (v.g ? IND_GRASPED : 0u);
+      err |= isnan(v.force) ? ERR_FORCE : 0u;
+      break;
+    case TL_PLACE: {
+      const bool in = LE(v.dist, c.rd_goal, c.goal_radius);
+      if (!over && !v.g && isnan(v.dist)) err |= ERR_SUCC;
+      succ = !over && !v.g && in && at_rest(c, v, true);
+      ind |= (v.g ? IND_GRASPED : 0u) | (in ? IND_A : 0u) |
+             (GT(v.dist, c.rd_goal, c.goal_radius) ? IND_B : 0u);
+      err |= isnan(v.dist) ? ERR_DIST : 0u;
+      break;
+    }
+    case TL_OPEN: {
+      const bool has_art = c.art_kind != TL_ART_NONE;
+      if (!over && (!has_art || isnan(v.art))) err |= ERR_SUCC;
+      const bool open = GE(v.art, c.ru_open, c.open_cut);
+      succ = !over && has_art && open && at_rest(c, v, true);
+      ind |= (GT(v.force, c.rd_contact, c.contact_eps) ? IND_CONTACT : 0u) |
+             (open ? IND_A : 0u) |
+             (GE(v.art, c.ru_slight_open, c.slight_open_cut) ? IND_B : 0u);
+      err |= (isnan(v.force) ? ERR_FORCE : 0u) | (isnan(v.art) ? ERR_ART : 0u);
+      break;
+    }
+    default: {  // TL_CLOSE
+      const bool has_art = c.art_kind != TL_ART_NONE;
+      if (!over && (!has_art || isnan(v.art))) err |= ERR_SUCC;
+      const bool closed = LE(v.art, c.rd_closed, c.closed_cut);
+      succ = !over && has_art && closed && at_rest(c, v, true);
+      ind |= (GT(v.force, c.rd_contact, c.contact_eps) ? IND_CONTACT : 0u) |
+             (closed ? IND_A : 0u) | (LT(v.art, sc_ru, sc_d) ? IND_B : 0u);
+      err |= (isnan(v.force) ? ERR_FORCE : 0u) | (isnan(v.art) ? ERR_ART : 0u);
+      break;
+    }
+  }
+  if (succ) ind |= IND_SUCCESS;
+}
+
+// edge tests of extract_events in EVENT_ORDER bit order
+__device__ __forceinline__ uint32_t edge_mask(int subtask, uint32_t p, uint32_t c) {
+  const uint32_t rise = ~p & c, fall = p & ~c;
+  const uint32_t C = (rise & IND_CONTACT) ? 1u : 0u;
+  const uint32_t G = (rise & IND_GRASPED) ? 1u : 0u;
+  const uint32_t D = (fall & IND_GRASPED) ? 1u : 0u;
+  const uint32_t S = (rise & IND_SUCCESS) ? 1u : 0u;
+  const uint32_t X = ((p & IND_CUM_LE) && (c & IND_CUM_GT)) ? 1u : 0u;
+  const uint32_t Ar = (rise & IND_A) ? 1u : 0u, Af = (fall & IND_A) ? 1u : 0u;
+  const uint32_t Br = (rise & IND_B) ? 1u : 0u;
+  switch (subtask) {
+    case TL_PICK:  // Contact, Grasped, Dropped, Success, ExcessiveCollisions
+      return C | (G << 1) | (D << 2) | (S << 3) | (X << 4);
+    case TL_PLACE: {  // Grasped, ObjAtGoal, RAG, ROG, ObjLeftGoal, Success, X
+      const uint32_t oag = ((p & IND_B) && (c & IND_A)) ? 1u : 0u;
+      const uint32_t olg = ((p & IND_A) && (c & IND_B)) ? 1u : 0u;
+      const uint32_t rag = (D && (c & IND_A)) ? 1u : 0u;
+      const uint32_t rog = (D && !(c & IND_A)) ? 1u : 0u;
+      return G | (oag << 1) | (rag << 2) | (rog << 3) | (olg << 4) | (S << 5) | (X << 6);
+    }
+    default:  // Open: Contact, Opened, SlightlyOpened, Closed, Success, X
+              // Close: Contact, Closed, SlightlyClosed, Open, Success, X
+      return C | (Ar << 1) | (Br << 2) | (Af << 3) | (S << 4) | (X << 5);
+  }
+}
+
+__device__ __forceinline__ int alphabet_size(int subtask) {
+  return subtask == TL_PICK ? 5 : subtask == TL_PLACE ? 7 : 6;
+}
+
+// warp-uniform running label state of one episode
+struct LState {
+  int size;
+  int last[7];
+  uint32_t prev_ind;
+  uint32_t err_any;
+};
+
+__device__ __forceinline__ void lstate_init(LState& S) {
+  S.size = 0;
+#pragma unroll
+  for (int k = 0; k < 7; k++) S.last[k] = -1;
+  S.prev_ind = 0;
+  S.err_any = 0;
+}
+
+// fold one chunk's per-lane event masks into the running state
+__device__ __forceinline__ void lstate_fold(LState& S, uint32_t mask, uint32_t err) {
+  const int cnt = __popc(mask);
+  const int incl = warp_incl_scan(cnt);
+  const int excl = incl - cnt;
+#pragma unroll
+  for (int k = 0; k < 7; k++) {
+    const unsigned bal = __ballot_sync(kFull, (mask >> k) & 1u);
+    if (bal) {
+      const int L = 31 - __clz(bal);
+      const int exL = __shfl_sync(kFull, excl, L);
+      const uint32_t mL = __shfl_sync(kFull, mask, L);
+      S.last[k] = S.size + exL + __popc(mL & ((1u << k) - 1u));
+    }
+  }
+  S.size += __shfl_sync(kFull, incl, 31);
+  S.err_any |= __reduce_or_sync(kFull, err);
+}
+
+// ---- classification (modes.py) ---------------------------------------------
+struct Sig {
+  int size, c, g, d, oag, rag, rog, olg, opened, so, closed, sc, open, s, x;
+  double d0;
+  bool d0_none, s1;
+};
+
+__device__ __forceinline__ void sig_clear(Sig& z) {
+  z.size = 0;
+  z.c = z.g = z.d = z.oag = z.rag = z.rog = z.olg = z.opened = z.so = z.closed =
+      z.sc = z.open = z.s = z.x = -1;
+  z.d0 = 0.0;
+  z.d0_none = false;
+  z.s1 = false;
+}
+
+__device__ __forceinline__ void sig_set(Sig& z, int kind, int idx) {
+  switch (kind) {
+    case TL_EV_CONTACT: z.c = idx; break;
+    case TL_EV_GRASPED: z.g = idx; break;
+    case TL_EV_DROPPED: z.d = idx; break;
+    case TL_EV_OBJ_AT_GOAL: z.oag = idx; break;
+    case TL_EV_RELEASED_AT_GOAL: z.rag = idx; break;
+    case TL_EV_RELEASED_OUTSIDE_GOAL: z.rog = idx; break;
+    case TL_EV_OBJ_LEFT_GOAL: z.olg = idx; break;
+    case TL_EV_OPENED: z.opened = idx; break;
+    case TL_EV_SLIGHTLY_OPENED: z.so = idx; break;
+    case TL_EV_CLOSED: z.closed = idx; break;
+    case TL_EV_SLIGHTLY_CLOSED: z.sc = idx; break;
+    case TL_EV_OPEN: z.open = idx; break;
+    case TL_EV_SUCCESS: z.s = idx; break;
+    case TL_EV_EXCESSIVE_COLLISIONS: z.x = idx; break;
+  }
+}
+
+__device__ __forceinline__ void sig_from_state(Sig& z, int subtask, const LState& S) {
+  sig_clear(z);
+  z.size = S.size;
+#pragma unroll
+  for (int k = 0; k < 7; k++)
+    if (k < alphabet_size(subtask)) sig_set(z, kAlpha[subtask][k], S.last[k]);
+  z.s1 = z.size == 3 && z.c == 0 && z.g == 1 && z.s == 2;
+}
+
+#define TL_GOAL_RADIUS 0.15 /* modes.py:65 literal, independent of thresholds */
+
+// one builtin rule predicate (modes.py:68-205); 1/0 or -status
+__device__ int rule_pred(int m, const Sig& z) {
+  const bool exc = z.x >= 0;
+#define D0_LE(out)                                   \
+  do {                                               \
+    if (z.d0_none) return -TL_ERR_D0_NONE_LE;        \
+    out = z.d0 <= TL_GOAL_RADIUS;                    \
+  } while (0)
+#define D0_GT(out)                                   \
+  do {                                               \
+    if (z.d0_none) return -TL_ERR_D0_NONE_GT;        \
+    out = z.d0 > TL_GOAL_RADIUS;                     \
+  } while (0)
+  bool t;
+  switch (m) {
+    case 0: return z.s1;
+    case 1: return !exc && z.d <= z.g;
+    case 2: return !exc && z.d > z.g;
+    case 3: case 4: return exc;
+    case 5: return z.size == 0;
+    case 6: return z.c >= 0 && z.g < 0 && z.d < 0;
+    case 7: return z.d >= 0 && z.d > z.g;
+    case 8: return 1;
+    case 9:
+      if (!(z.size <= 4)) return 0;
+      if (!(z.rag >= 0)) { D0_LE(t); if (!t) return 0; }
+      return z.olg <= z.oag && !exc;
+    case 10:
+      if (!(z.size <= 4)) return 0;
+      if (!(z.rog >= 0)) { D0_GT(t); if (!t) return 0; }
+      return z.olg <= z.oag && !exc;
+    case 11: return z.oag < z.olg && !exc;
+    case 12: return z.size > 4 && z.oag >= z.olg && !exc;
+    case 13: case 14: return exc;
+    case 15: return z.size == 0;
+    case 16: return z.size > 0 && z.oag < 0;
+    case 17: {
+      if (z.oag < 0) return 0;
+      bool lat = false;
+      if (z.size <= 2) D0_LE(lat);
+      if (!lat) lat = z.rag > z.rog && z.rag > z.g;
+      return lat && z.olg > z.oag;
+    }
+    case 18: {
+      if (z.oag < 0) return 0;
+      bool lat = false;
+      if (z.size <= 2) D0_GT(lat);
+      if (!lat) lat = z.rog > z.rag && z.rog > z.g;
+      return lat && z.olg > z.oag;
+    }
+    case 19: return z.oag >= 0 && z.g > z.rag && z.g > z.rog;
+    case 20: return 1;
+    case 21: return !exc && z.opened >= z.closed;
+    case 22: return !exc && z.opened < z.closed;
+    case 23: case 24: return exc;
+    case 25: return z.c < 0;
+    case 26: return z.closed >= 0 && z.closed > z.opened && z.closed > z.so;
+    case 27: return z.so > z.opened && z.so > z.closed;
+    case 28: return z.opened >= 0;
+    case 29: return 1;
+    case 30: return !exc && z.closed >= z.open;
+    case 31: return !exc && z.closed < z.open;
+    case 32: case 33: return exc;
+    case 34: return z.c < 0;
+    case 35: return z.closed >= 0 && z.open > z.closed && z.open > z.sc;
+    case 36: return z.sc > z.closed && z.sc > z.open;
+    case 37: return z.closed >= 0;
+    case 38: return 1;
+  }
+#undef D0_LE
+#undef D0_GT
+  return 0;
+}
+
+__device__ __forceinline__ bool success_at_end_mode(int m) {  // modes.py:226-232
+  return m == 0 || m == 1 || m == 9 || m == 10 || m == 12 || m == 21 || m == 30;
+}
+
+// classify (modes.py:235-253): mode id (>=0) or -status; flags out
+__device__ int classify_sig(int subtask, const Sig& z, const tl_rules& rules,
+                            uint8_t& flags) {
+  const bool so = z.s >= 0;
+  const int b = so ? 0 : 1;
+  const int cnt = rules.count[subtask][b];
+  flags = so ? 1u : 0u;
+  for (int i = 0; i < cnt; i++) {
+    const int m = rules.ids[subtask][b][i];
+    const int r = rule_pred(m, z);
+    if (r < 0) return r;
+    if (r) {
+      if (success_at_end_mode(m)) flags |= 2u;
+      return m;
+    }
+  }
+  return -TL_ERR_MODE_COVERAGE;
+}
+
+// final per-episode status precedence = evaluation order of extract_events
+// (events.py:105 success loop, then :112/:127/:153/:172 per-subtask lists)
+__device__ __forceinline__ int label_status(const tl_cset& c, uint32_t err_any) {
+  const bool art_sub = c.subtask == TL_OPEN || c.subtask == TL_CLOSE;
+  const bool has_art = c.art_kind != TL_ART_NONE;
+  if (err_any & ERR_SUCC) {
+    if (c.subtask == TL_PLACE) return TL_ERR_NAN_SUCCESS_DIST;
+    return has_art ? TL_ERR_NAN_ART : TL_ERR_MISSING_ART;
+  }
+  if (c.subtask != TL_PLACE && (err_any & ERR_FORCE)) return TL_ERR_NAN_FORCE;
+  if (c.subtask == TL_PLACE && (err_any & ERR_DIST)) return TL_ERR_NAN_PLACE_DIST;
+  if (art_sub && !has_art) return TL_ERR_MISSING_ART;
+  if (art_sub && (err_any & ERR_ART)) return TL_ERR_NAN_ART;
+  return TL_OK;
+}
+
+// Finalise an episode: status + classify; writes the label (lane 0 only).
+__device__ __forceinline__ void finish_label(const tl_cset& c, const LState& S,
+                                             double d0, const tl_rules& rules,
+                                             tl_label* out) {
+  tl_label L;
+  L.status = label_status(c, S.err_any);
+  L.n_events = 0;
+  L.err_index = -1;
+  L.subtask = (uint8_t)c.subtask;
+  L.mode = 255;
+  L.flags = 0;
+  L.pad = 0;
+  L.d0 = c.subtask == TL_PLACE ? d0 : __longlong_as_double(0x7ff8000000000000ll);
+  if (L.status == TL_OK) {
+    Sig z;
+    sig_from_state(z, c.subtask, S);
+    z.d0 = d0;
+    uint8_t fl = 0;
+    const int m = classify_sig(c.subtask, z, rules, fl);
+    L.n_events = S.size;  // events exist even when no mode rule matches
+    if (m < 0) {
+      L.status = -m;
+      L.flags = z.s >= 0 ? 1 : 0;
+    } else {
+      L.mode = (uint8_t)m;
+      L.flags = fl;
+    }
+  }
+  if (lane_id() == 0) *out = L;
+}
+
+// stage one cset into a per-warp shared slot
+__device__ __forceinline__ void stage_cset(tl_cset* dst, const tl_cset* src) {
+  static_assert(sizeof(tl_cset) % 4 == 0, "cset size");
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  for (int i = lane_id(); i < (int)(sizeof(tl_cset) / 4); i += 32) d[i] = __ldg(s + i);
+  __syncwarp();
+}
+
+// Close: slightly-closed cut from records[0].art_q (events.py:174-176)
+__device__ __forceinline__ void close_cut(const tl_cset& c, double a0, float& ru, double& d) {
+  d = __dsub_rn(a0, c.scf_span);
+  ru = __double2float_ru(d);
+}
+
+// ---- K1: label_records -------------------------------------------------------
+constexpr int kLabelWarps = 8;
+
+template <typename T, int DOFMAX>
+__global__ void __launch_bounds__(kLabelWarps * 32)
+    k_label(tl_records R, int n_env, const int32_t* __restrict__ env_cset,
+            const tl_cset* __restrict__ csets, tl_rules rules,
+            uint8_t* __restrict__ step_mask, uint8_t* __restrict__ step_success,
+            tl_label* __restrict__ labels) {
+  __shared__ tl_cset s_cs[kLabelWarps];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const T* __restrict__ P = reinterpret_cast<const T*>(R.planes);
+  const int64_t stride = R.plane_stride;
+  const int dof = R.dof;
+  for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
+    stage_cset(&s_cs[warp], &csets[env_cset[e]]);
+    const tl_cset& c = s_cs[warp];
+    const int64_t rs = R.rec_start[e];
+    const int n = R.n_rec[e];
+    LState S;
+    lstate_init(S);
+    if (n < 2) {  // events.py:96-97
+      if (lane == 0) {
+        tl_label L;
+        L.status = TL_ERR_TOO_SHORT; L.n_events = 0; L.err_index = -1;
+        L.subtask = (uint8_t)c.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
+        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
+        labels[e] = L;
+      }
+      if (step_success) {  // predicate values are still defined per record
+        // fallthrough below handles n == 1 through the generic loop
+      } else {
+        continue;
+      }
+    }
+    const int f0 = 2 * dof;
+    double d0 = 0.0;
+    float sc_ru = 0.f;
+    double sc_d = 0.0;
+    if (c.subtask == TL_PLACE) d0 = (double)P[(f0 + 5) * stride + rs];
+    if (c.subtask == TL_CLOSE && n > 0) close_cut(c, (double)P[(f0 + 8) * stride + rs], sc_ru, sc_d);
+    for (int t0 = 0; t0 < n; t0 += 32) {
+      const int t = t0 + lane;
+      const bool valid = t < n;
+      const int64_t r = rs + t;
+      RecV<T> v;
+      uint32_t ind = 0, err = 0;
+      if (valid) {
+        v.der = P[(f0 + 4) * stride + r];
+        v.cum = P[(f0 + 7) * stride + r];
+        v.vx = P[(f0 + 1) * stride + r];
+        v.vy = P[(f0 + 2) * stride + r];
+        v.om = P[(f0 + 3) * stride + r];
+        // Python-max of |q_i - rest_i| and of |qd_i|
+        T m = 0, mq = 0;
+        double md = 0.0;
+#pragma unroll
+        for (int i = 0; i < DOFMAX; i++) {
+          if (i < dof) {
+            const T q = P[i * stride + r];
+            const T qd = P[(dof + i) * stride + r];
+            const T aq = tabs(q), aqd = tabs(qd);
+            m = i == 0 ? aq : pymax_step(m, aq);
+            mq = i == 0 ? aqd : pymax_step(mq, aqd);
+            if (!c.rest_zero) {
+              const double dv = fabs(__dsub_rn((double)q, c.rest_arm[i]));
+              md = i == 0 ? dv : pymax_step(md, dv);
+            }
+          }
+        }
+        v.jm = m;
+        v.qdm = mq;
+        v.jm_d = md;
+        v.tor = 0; v.dist = 0; v.force = 0; v.art = 0; v.g = false;
+        if (c.subtask == TL_PICK) {
+          v.force = P[(f0 + 6) * stride + r];
+          v.g = R.grasped[r] != 0;
+        } else if (c.subtask == TL_PLACE) {
+          v.tor = P[f0 * stride + r];
+          v.dist = P[(f0 + 5) * stride + r];
+          v.g = R.grasped[r] != 0;
+        } else {
+          v.tor = P[f0 * stride + r];
+          v.force = P[(f0 + 6) * stride + r];
+          v.art = P[(f0 + 8) * stride + r];
+        }
+        record_bits(c, v, sc_ru, sc_d, ind, err);
+        if (step_success) step_success[r] = (err & ERR_SUCC) ? 2 : ((ind & IND_SUCCESS) ? 1 : 0);
+      }
+      uint32_t prev = __shfl_up_sync(kFull, ind, 1);
+      if (lane == 0) prev = S.prev_ind;
+      const uint32_t mask = (valid && t > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
+      if (valid && step_mask) step_mask[r] = (uint8_t)mask;
+      lstate_fold(S, mask, valid ? err : 0u);
+      S.prev_ind = __shfl_sync(kFull, ind, 31);
+    }
+    if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
+  }
+}
+
+// ---- K2: event list emission --------------------------------------------------
+constexpr int kEmitWarps = 8;
+
+__global__ void __launch_bounds__(kEmitWarps * 32)
+    k_emit(const uint8_t* __restrict__ step_mask, const int64_t* __restrict__ rec_start,
+           const int32_t* __restrict__ n_rec, const tl_label* __restrict__ labels,
+           const int64_t* __restrict__ ev_off, int n_env, uint8_t* __restrict__ ev_kind,
+           int32_t* __restrict__ ev_t) {
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  for (int e = blockIdx.x * kEmitWarps + warp; e < n_env; e += gridDim.x * kEmitWarps) {
+    if (labels[e].n_events == 0) continue;
+    const int sub = labels[e].subtask;
+    const int64_t rs = rec_start[e];
+    const int n = n_rec[e];
+    int64_t base = ev_off[e];
+    for (int t0 = 0; t0 < n; t0 += 32) {
+      const int t = t0 + lane;
+      const uint32_t mask = t < n ? step_mask[rs + t] : 0u;
+      const int cnt = __popc(mask);
+      const int incl = warp_incl_scan(cnt);
+      int64_t pos = base + incl - cnt;
+      uint32_t m = mask;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        ev_kind[pos] = kAlpha[sub][k];
+        ev_t[pos] = t;
+        pos++;
+      }
+      base += __shfl_sync(kFull, incl, 31);
+    }
+  }
+}
+
+// ---- scan of event counts -------------------------------------------------------
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ int64_t block_excl_scan64(int64_t v, int64_t* sh, int64_t& total) {
+  // sh: 32 slots
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int64_t u = __shfl_up_sync(kFull, x, d);
+    if (lane >= d) x += u;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int64_t u = __shfl_up_sync(kFull, w, d);
+      if (lane >= d) w += u;
+    }
+    sh[lane] = w;
+  }
+  __syncthreads();
+  const int64_t wbase = warp ? sh[warp - 1] : 0;
+  total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return wbase + x - v;
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    k_scan_tiles(const tl_label* __restrict__ labels, int n, int64_t* __restrict__ ev_off,
+                 int64_t* __restrict__ tile_sum) {
+  __shared__ int64_t sh[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  int64_t v = 0;
+  if (i < n) v = labels[i].n_events;  // 0 whenever extraction failed
+  int64_t total;
+  const int64_t ex = block_excl_scan64(v, sh, total);
+  if (i < n) ev_off[i] = ex;
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    k_scan_sums(int64_t* __restrict__ tile_sum, int n_tiles, int64_t* __restrict__ ev_off, int n) {
+  __shared__ int64_t sh[32];
+  int64_t carry = 0;
+  for (int b = 0; b < n_tiles; b += kScanBlock) {
+    const int i = b + threadIdx.x;
+    const int64_t v = i < n_tiles ? tile_sum[i] : 0;
+    int64_t total;
+    const int64_t ex = block_excl_scan64(v, sh, total);
+    if (i < n_tiles) tile_sum[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) ev_off[n] = carry;
+}
+
+__global__ void k_scan_add(int64_t* __restrict__ ev_off, const int64_t* __restrict__ tile_off, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ev_off[i] += tile_off[i / kScanBlock];
+}
+
+// ---- classify given event lists (thread per list) --------------------------------
+__global__ void k_classify_events(const uint8_t* __restrict__ ev_kind,
+                                  const int64_t* __restrict__ ev_off,
+                                  const uint8_t* __restrict__ subtask,
+                                  const double* __restrict__ d0,
+                                  const uint8_t* __restrict__ d0_none, int n,
+                                  tl_rules rules, tl_label* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int sub = subtask[e];
+  const int64_t a = ev_off[e], b = ev_off[e + 1];
+  Sig z;
+  sig_clear(z);
+  z.size = (int)(b - a);
+  for (int64_t i = a; i < b; i++) sig_set(z, ev_kind[i], (int)(i - a));
+  z.s1 = z.size == 3 && ev_kind[a] == TL_EV_CONTACT && ev_kind[a + 1] == TL_EV_GRASPED &&
+         ev_kind[a + 2] == TL_EV_SUCCESS;
+  z.d0 = d0 ? d0[e] : 0.0;
+  z.d0_none = d0_none ? d0_none[e] != 0 : false;
+  tl_label L;
+  L.err_index = -1;
+  L.subtask = (uint8_t)sub;
+  L.pad = 0;
+  L.d0 = z.d0;
+  uint8_t fl = 0;
+  const int m = classify_sig(sub, z, rules, fl);
+  L.status = m < 0 ? -m : TL_OK;
+  L.mode = m < 0 ? 255 : (uint8_t)m;
+  L.flags = m < 0 ? (z.s >= 0 ? 1 : 0) : fl;
+  L.n_events = z.size;
+  out[e] = L;
+}
+
+// ---- K6: mode histogram ------------------------------------------------------------
+__global__ void k_mode_hist(const tl_label* __restrict__ labels, int n,
+                            unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[TL_N_MODES];
+  for (int i = threadIdx.x; i < TL_N_MODES; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const tl_label L = labels[i];
+    if (L.status == TL_OK && L.mode < TL_N_MODES) atomicAdd(&h[L.mode], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TL_N_MODES; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+}  // namespace tl
+
+namespace tl {
+
+// ---- per-record predicate evaluation (predicates.py:16-99) -------------------
+template <typename T, int DOFMAX>
+__global__ void __launch_bounds__(kLabelWarps * 32)
+    k_predicates(tl_records R, int n_env, const int32_t* __restrict__ env_cset,
+                 const tl_cset* __restrict__ csets, const double* __restrict__ a0v,
+                 uint8_t* __restrict__ bits, uint8_t* __restrict__ errs,
+                 double* __restrict__ jmax) {
+  __shared__ tl_cset s_cs[kLabelWarps];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const T* __restrict__ P = reinterpret_cast<const T*>(R.planes);
+  const int64_t stride = R.plane_stride;
+  const int dof = R.dof, f0 = 2 * dof;
+  for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
+    stage_cset(&s_cs[warp], &csets[env_cset[e]]);
+    const tl_cset& c = s_cs[warp];
+    const int64_t rs = R.rec_start[e];
+    const int n = R.n_rec[e];
+    float sc_ru = 0.f;
+    double sc_d = 0.0;
+    if (c.subtask == TL_CLOSE && n > 0)
+      close_cut(c, a0v ? a0v[e] : (double)P[(f0 + 8) * stride + rs], sc_ru, sc_d);
+    for (int t = lane; t < n; t += 32) {
+      const int64_t r = rs + t;
+      RecV<T> v;
+      v.der = P[(f0 + 4) * stride + r];
+      v.cum = P[(f0 + 7) * stride + r];
+      v.vx = P[(f0 + 1) * stride + r];
+      v.vy = P[(f0 + 2) * stride + r];
+      v.om = P[(f0 + 3) * stride + r];
+      v.tor = P[f0 * stride + r];
+      v.dist = P[(f0 + 5) * stride + r];
+      v.force = P[(f0 + 6) * stride + r];
+      v.art = P[(f0 + 8) * stride + r];
+      v.g = R.grasped[r] != 0;
+      T m = 0, mq = 0;
+      double md = 0.0;
+#pragma unroll
+      for (int i = 0; i < DOFMAX; i++) {
+        if (i < dof) {
+          const T q = P[i * stride + r];
+          const T qd = P[(dof + i) * stride + r];
+          m = i == 0 ? tabs(q) : pymax_step(m, tabs(q));
+          mq = i == 0 ? tabs(qd) : pymax_step(mq, tabs(qd));
+          const double dv = fabs(__dsub_rn((double)q, c.rest_arm[i]));
+          md = i == 0 ? dv : pymax_step(md, dv);
+        }
+      }
+      v.jm = m;
+      v.qdm = mq;
+      v.jm_d = md;
+      uint32_t ind, err;
+      record_bits(c, v, sc_ru, sc_d, ind, err);
+      const bool stat = LE(v.qdm, c.rd_static_qd, c.static_qd) &&
+                        LE(tabs(v.vx), c.rd_static_v, c.static_v) &&
+                        LE(tabs(v.vy), c.rd_static_v, c.static_v) &&
+                        LE(tabs(v.om), c.rd_static_om, c.static_om);
+      // grasped bit is reported for every subtask
+      ind = (ind & ~IND_GRASPED) | (v.g ? IND_GRASPED : 0u) |
+            (GT(v.force, c.rd_contact, c.contact_eps) ? IND_CONTACT : 0u);
+      if (bits) bits[r] = (uint8_t)(ind | (stat ? 128u : 0u));
+      if (errs) errs[r] = (uint8_t)(err | (isnan(v.force) ? ERR_FORCE : 0u) |
+                                    (isnan(v.dist) ? ERR_DIST : 0u) | (isnan(v.art) ? ERR_ART : 0u));
+      if (jmax) jmax[r] = md;
+    }
+  }
+}
+
+}  // namespace tl
+
+namespace tl {
+
+// ---- generic int32 exclusive scan (record counts -> compact offsets) ---------
+__global__ void __launch_bounds__(kScanBlock)
+    k_scan_i32_tiles(const int32_t* __restrict__ in, int n, int64_t* __restrict__ out,
+                     int64_t* __restrict__ tile_sum) {
+  __shared__ int64_t sh[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const int64_t v = i < n ? in[i] : 0;
+  int64_t total;
+  const int64_t ex = block_excl_scan64(v, sh, total);
+  if (i < n) out[i] = ex;
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
+}
+
+// ---- compaction of a padded record layout (one warp per episode) -------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_compact(tl_records src, int n_env, const int64_t* __restrict__ dst_start, tl_records dst,
+              int n_planes) {
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const T* __restrict__ sp = reinterpret_cast<const T*>(src.planes);
+  T* __restrict__ dp = reinterpret_cast<T*>(dst.planes);
+  for (int e = blockIdx.x * 8 + warp; e < n_env; e += gridDim.x * 8) {
+    const int64_t a = src.rec_start[e], b = dst_start[e];
+    const int n = src.n_rec[e];
+    for (int t = lane; t < n; t += 32) {
+      for (int f = 0; f < n_planes; f++) dp[f * dst.plane_stride + b + t] = sp[f * src.plane_stride + a + t];
+      dst.grasped[b + t] = src.grasped[a + t];
+    }
+    if (lane == 0) {
+      dst.rec_start[e] = b;
+      dst.n_rec[e] = n;
+    }
+  }
+}
+
+}  // namespace tl

@@ -1,0 +1,743 @@
+// tl_synth.cuh -- batched env reset/step: random_script + realize, fused
+// with online labelling (one warp per episode).
+//
+// Reference (paths under /root/reference/pkg/src/trajlab/):
+//   synth.py:100-162  _Realizer.__init__  (= reset)
+//   synth.py:166-196  _emit / _advance_cum
+//   synth.py:205-296  _apply              (= step(action))
+//   synth.py:298-348  run / _build / realize
+//   synth.py:363-515  random_script / fuzz
+//
+// Every record t >= 1 is one env step: advance_cum (1 draw before the
+// ExcessiveCollisions jump), apply (1 draw for ObjAtGoal/ObjLeftGoal) and
+// emit (2*dof+5 draws unless at rest).  Which draws happen depends only on
+// the script, not on drawn values, so a per-step plan (lane 0, O(steps))
+// fixes the MT word offset of every record; the 32 lanes of the warp then
+// generate 32 records at once from a shared ring of tempered MT words.
+// Only cum_robot_force is a true serial f64 recurrence (lane 0, 4 ops per
+// record).  Object distance draws and their feasibility checks happen at
+// the owning event record.
+#pragma once
+#include "tl_label.cuh"
+
+namespace tl {
+
+constexpr int kRingWords = 2048;  // >= 32 records * 42 words + 623
+constexpr uint32_t kRingMask = kRingWords - 1;
+constexpr int kMaxSteps = 64;     // script steps planned per window
+constexpr int kSynthWarps = 4;
+
+struct StepSt {          // realizer state after a step (index s+1); [0] = before
+  float force, art;      // record values (f32)
+  uint8_t grasped, at_rest, exc, level;
+  int16_t last_draw;     // window-local step of the latest dist draw, -1 = carry
+  int16_t pad;
+};
+
+struct SynthWarp {
+  uint32_t mt[kMtN];            // realize RNG state
+  uint32_t ring[kRingWords];    // tempered words; [0, 624) = script RNG state first
+  int32_t gap[kMaxSteps];
+  int32_t tau[kMaxSteps];       // record index of step s's event
+  int32_t W[kMaxSteps + 1];     // word offset of segment s's first record
+  int32_t hw[kMaxSteps + 1];    // words per hold record in segment s
+  StepSt st[kMaxSteps + 1];
+  double dist_after[kMaxSteps];
+  double radv[32];
+  float cum32[32];
+  uint8_t kind[kMaxSteps];
+  uint8_t sflag[kMaxSteps];     // bit0 dist draw at the event
+  uint8_t rflag[32];            // bit0 advance draw, bit1 ExcessiveCollisions applied
+  int32_t misc[16];
+  tl_cset cs;                   // labelling constants (staged)
+};
+
+struct RzConst {
+  int kind, has_art, has_goal, has_force, dof, ne;
+  double limit, L09, L105, goal, qmin, qmax, closed_thresh, sc_thresh,
+      lv_low, lv_slight, lv_open, a_q0, sc_art;
+  int band_valid;
+};
+
+struct SynthParams {
+  // fuzz inputs
+  const int64_t* seeds;
+  int32_t fuzz_subtask;
+  tl_fuzz_cfg cfg;
+  uint8_t* script_kind;
+  int32_t* script_gap;
+  tl_script* scripts_out;
+  // realize inputs
+  const tl_script* scripts;
+  const uint8_t* step_kind;
+  const int32_t* step_gap;
+  // common
+  int32_t n_env;
+  int32_t cap_per_env;
+  tl_thresholds th;
+  const tl_cset* label_csets;   // [subtask*3 + art_kind]
+  tl_rules rules;
+  tl_records out;
+  uint8_t* step_mask;
+  tl_label* labels;
+};
+
+__device__ __forceinline__ bool in_alpha(int k, int ev) {
+#pragma unroll
+  for (int i = 0; i < 7; i++)
+    if (kAlpha[k][i] == ev) return true;
+  return false;
+}
+
+// choices(pop, weights)[0] (Lib/random.py): accumulate + bisect_right
+__device__ int choices_idx(MtLane& R, const double* w, int n) {
+  double cum[4];
+  double acc = 0.0;
+  for (int i = 0; i < n; i++) {
+    acc = i == 0 ? w[0] : __dadd_rn(acc, w[i]);
+    cum[i] = acc;
+  }
+  const double total = __dadd_rn(cum[n - 1], 0.0);
+  const double x = __dmul_rn(R.random(), total);
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (x < cum[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// random_script (synth.py:363-507), lane 0.  Returns n_steps or -1 when the
+// script does not fit kMaxSteps.
+__device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
+                             uint8_t* sk, int32_t* sg, tl_script& sc) {
+  int n = 0;
+  bool overflow = false;
+  auto push = [&](int ev) {
+    const int32_t g = R.randint(1, cfg.max_gap);
+    if (n < kMaxSteps) { sk[n] = (uint8_t)ev; sg[n] = g; n++; } else overflow = true;
+  };
+  sc.tail = R.randint(1, cfg.max_tail);                                  // :372
+  sc.initial_grasped = 0;
+  sc.initial_contact = 0;
+  sc.initial_dist_obj_goal = 0.5;
+  sc.initial_level = TL_LVL_LOW;
+  sc.art_kind = TL_ART_FRIDGE;
+  sc.arm_dof = 7;
+  sc.subtask = kind;
+  if (kind == TL_OPEN || kind == TL_CLOSE)                               // :374-376
+    sc.art_kind = R.randbelow(2) ? TL_ART_DRAWER : TL_ART_FRIDGE;
+  if (kind == TL_PICK) {                                                 // :379-381
+    sc.initial_contact = R.random() < 0.25;
+    sc.initial_grasped = sc.initial_contact && R.random() < 0.4;
+  } else if (kind == TL_PLACE) {                                         // :382-386
+    sc.initial_grasped = R.random() < 0.8;
+    sc.initial_dist_obj_goal = R.random() < 0.7 ? R.uniform(0.3, 0.9) : R.uniform(0.02, 0.12);
+  } else {                                                               // :387-392
+    const double w[3] = {0.85, 0.1, 0.05};
+    const int c = choices_idx(R, w, 3);
+    if (kind == TL_OPEN) sc.initial_level = c == 0 ? TL_LVL_LOW : c == 1 ? TL_LVL_SLIGHT : TL_LVL_OPEN;
+    else sc.initial_level = c == 0 ? TL_LVL_HIGH : c == 1 ? TL_LVL_SLIGHT : TL_LVL_CLOSED;
+  }
+  bool grasped = sc.initial_grasped, contact = sc.initial_contact;       // :394-403
+  bool in_goal = sc.initial_dist_obj_goal <= 0.15;
+  int level = sc.initial_level;
+  bool band = true;
+  if (kind == TL_CLOSE) {
+    level = sc.initial_level == TL_LVL_CLOSED ? TL_LVL_CLOSED : TL_LVL_OPEN;
+    band = sc.initial_level != TL_LVL_CLOSED;
+  }
+  bool contact_used = contact;                                           // :461
+  const long n_target = (long)rint(__dmul_rn((double)R.randint(0, cfg.max_events), cfg.edge_density));
+  for (long it = 0; it < n_target; it++) {                               // :464-474
+    int mv[3], nm = 0;
+    if (kind == TL_PICK) {
+      if (!contact) mv[nm++] = TL_EV_CONTACT;
+      if (!grasped && contact) mv[nm++] = TL_EV_GRASPED;
+      if (grasped) mv[nm++] = TL_EV_DROPPED;
+    } else if (kind == TL_PLACE) {
+      mv[nm++] = !grasped ? TL_EV_GRASPED : in_goal ? TL_EV_RELEASED_AT_GOAL : TL_EV_RELEASED_OUTSIDE_GOAL;
+      mv[nm++] = in_goal ? TL_EV_OBJ_LEFT_GOAL : TL_EV_OBJ_AT_GOAL;
+    } else if (kind == TL_OPEN) {
+      mv[nm++] = TL_EV_CONTACT;
+      mv[nm++] = level == TL_LVL_LOW ? TL_EV_SLIGHTLY_OPENED : level == TL_LVL_SLIGHT ? TL_EV_OPENED : TL_EV_CLOSED;
+    } else {
+      mv[nm++] = TL_EV_CONTACT;
+      if (level == TL_LVL_OPEN) { if (band) mv[nm++] = TL_EV_SLIGHTLY_CLOSED; }
+      else if (level == TL_LVL_SLIGHT) mv[nm++] = TL_EV_CLOSED;
+      else mv[nm++] = TL_EV_OPEN;
+    }
+    if ((kind == TL_OPEN || kind == TL_CLOSE) && contact_used) {
+      int k = 0;
+      for (int i = 0; i < nm; i++) if (mv[i] != TL_EV_CONTACT) mv[k++] = mv[i];
+      nm = k;
+    }
+    if (!nm) break;
+    const int m = mv[R.randbelow((uint32_t)nm)];
+    if (m == TL_EV_CONTACT) contact_used = true;
+    push(m);
+    switch (m) {                                                         // :434-457
+      case TL_EV_CONTACT: contact = true; break;
+      case TL_EV_GRASPED: grasped = true; break;
+      case TL_EV_DROPPED: grasped = false; contact = false; break;
+      case TL_EV_RELEASED_AT_GOAL: case TL_EV_RELEASED_OUTSIDE_GOAL: grasped = false; break;
+      case TL_EV_OBJ_AT_GOAL: in_goal = true; break;
+      case TL_EV_OBJ_LEFT_GOAL: in_goal = false; break;
+      case TL_EV_SLIGHTLY_OPENED: level = TL_LVL_SLIGHT; break;
+      case TL_EV_OPENED: level = TL_LVL_OPEN; break;
+      case TL_EV_CLOSED: level = kind == TL_OPEN ? TL_LVL_LOW : TL_LVL_CLOSED; break;
+      case TL_EV_SLIGHTLY_CLOSED: level = TL_LVL_SLIGHT; break;
+      case TL_EV_OPEN: level = TL_LVL_OPEN; break;
+    }
+  }
+  bool feasible;                                                         // :476-483
+  if (kind == TL_PICK) feasible = grasped;
+  else if (kind == TL_PLACE) feasible = !grasped && in_goal;
+  else if (kind == TL_OPEN) feasible = level == TL_LVL_OPEN;
+  else feasible = level == TL_LVL_CLOSED;
+  const bool want = cfg.edge_density > 0 && R.random() < cfg.success_prob;  // :485
+  if (want && feasible) {
+    push(TL_EV_SUCCESS);
+    const double w[4] = {0.55, 0.2, 0.15, kind == TL_PLACE ? 0.1 : 0.0};
+    const int suffix = choices_idx(R, w, 4);
+    if (suffix == 1) {
+      // the dict literal at :493-496 evaluates gap() for all four subtasks
+      int32_t g[4];
+      for (int i = 0; i < 4; i++) g[i] = R.randint(1, cfg.max_gap);
+      const int brk = kind == TL_PICK ? TL_EV_DROPPED : kind == TL_PLACE ? TL_EV_OBJ_LEFT_GOAL
+                    : kind == TL_OPEN ? TL_EV_CLOSED : TL_EV_OPEN;
+      if (n < kMaxSteps) { sk[n] = (uint8_t)brk; sg[n] = g[kind]; n++; } else overflow = true;
+    } else if (suffix == 2) {
+      push(TL_EV_EXCESSIVE_COLLISIONS);
+    } else if (suffix == 3) {
+      push(TL_EV_OBJ_LEFT_GOAL);
+      push(TL_EV_OBJ_AT_GOAL);
+      push(TL_EV_SUCCESS);
+    }
+  } else if (cfg.edge_density > 0 && R.random() < 0.15) {               // :504-505
+    push(TL_EV_EXCESSIVE_COLLISIONS);
+  }
+  sc.n_steps = n;
+  return overflow ? -1 : n;
+}
+
+// _Realizer.__init__ constants (synth.py:104-148), all lanes
+__device__ __forceinline__ int realizer_init(RzConst& z, const tl_script& sc,
+                                             const tl_thresholds& th, int dof) {
+  const int k = sc.subtask;
+  z.kind = k;
+  z.dof = dof;
+  z.ne = 2 * dof + 5;
+  z.has_art = k == TL_OPEN || k == TL_CLOSE;
+  z.has_goal = k == TL_PLACE;
+  z.has_force = k != TL_PLACE;
+  z.limit = k == TL_PICK ? th.coll_pick : k == TL_PLACE ? th.coll_place : th.coll_artic;
+  z.L09 = __dmul_rn(z.limit, 0.9);
+  z.L105 = __dmul_rn(z.limit, 1.05);
+  z.goal = th.goal_radius;
+  z.qmin = z.qmax = z.closed_thresh = z.sc_thresh = 0.0;
+  z.lv_low = z.lv_slight = z.lv_open = z.a_q0 = z.sc_art = 0.0;
+  z.band_valid = 0;
+  if (z.has_art) {
+    if (sc.art_kind == TL_ART_FRIDGE) { z.qmin = 0.0; z.qmax = 1.6; }
+    else if (sc.art_kind == TL_ART_DRAWER) { z.qmin = 0.0; z.qmax = 0.5; }
+    else return TL_INF_INIT_LEVEL;
+    const double span = __dsub_rn(z.qmax, z.qmin);
+    const double ofrac = sc.art_kind == TL_ART_FRIDGE ? th.open_frac_fridge : th.open_frac_drawer;
+    const double open_t = __dadd_rn(__dmul_rn(ofrac, span), z.qmin);
+    z.closed_thresh = __dadd_rn(__dmul_rn(th.close_frac, span), z.qmin);
+    const double so_t = __dadd_rn(__dmul_rn(th.slightly_open_frac, span), z.qmin);
+    if (k == TL_OPEN) {
+      z.lv_low = z.qmin;
+      z.lv_slight = __ddiv_rn(__dadd_rn(so_t, open_t), 2.0);
+      z.lv_open = __ddiv_rn(__dadd_rn(open_t, z.qmax), 2.0);
+      if (sc.initial_level != TL_LVL_LOW && sc.initial_level != TL_LVL_SLIGHT &&
+          sc.initial_level != TL_LVL_OPEN) return TL_INF_INIT_LEVEL;
+    } else {
+      if (sc.initial_level == TL_LVL_HIGH) z.a_q0 = z.qmax;
+      else if (sc.initial_level == TL_LVL_SLIGHT) z.a_q0 = __dadd_rn(z.qmin, __dmul_rn(0.3, span));
+      else if (sc.initial_level == TL_LVL_CLOSED) z.a_q0 = z.qmin;
+      else return TL_INF_INIT_LEVEL;
+      z.sc_thresh = __dsub_rn(z.a_q0, __dmul_rn(th.slightly_close_frac, span));
+      z.band_valid = z.sc_thresh > z.closed_thresh;
+      z.sc_art = __ddiv_rn(__dadd_rn(z.sc_thresh, z.closed_thresh), 2.0);
+    }
+  }
+  if (k == TL_PICK && sc.initial_grasped && !sc.initial_contact)        // :154-155
+    return TL_INF_PICK_GRASPED_NO_CONTACT;
+  return TL_OK;
+}
+
+// deterministic part of _apply (synth.py:205-296) on the plan state.
+// Value-dependent checks (object distance vs goal) are deferred to the
+// event record (chunk pass).  Returns 0 or an InfeasibleScript code.
+struct PlanSt {
+  double force, art;
+  int grasped, at_rest, exc, level;
+};
+
+__device__ int plan_apply(const RzConst& z, PlanSt& p, int ev, int& draw) {
+  const int k = z.kind;
+  draw = 0;
+  if (!in_alpha(k, ev)) return TL_INF_NOT_IN_ALPHABET;
+  if (ev == TL_EV_EXCESSIVE_COLLISIONS) {
+    if (p.exc) return TL_INF_LIMIT_EXCEEDED;  // cum = 1.05*limit > limit
+    p.exc = 1;
+    return 0;
+  }
+  if (ev == TL_EV_SUCCESS) {
+    bool ok;
+    if (k == TL_PICK) ok = p.grasped;
+    else if (k == TL_PLACE) ok = !p.grasped;  // and dist <= goal (deferred)
+    else if (k == TL_OPEN) ok = p.level == TL_LVL_OPEN;
+    else ok = p.level == TL_LVL_CLOSED;
+    if (!ok || p.at_rest) return TL_INF_SUCCESS_UNREACHABLE;
+    p.at_rest = 1;
+    return 0;
+  }
+  p.at_rest = 0;
+  switch (ev) {
+    case TL_EV_CONTACT:
+      if (!z.has_force) return TL_INF_CONTACT_UNDEFINED;
+      if (p.force > 0) return TL_INF_CONTACT_AGAIN;
+      p.force = 1.2;
+      return 0;
+    case TL_EV_GRASPED:
+      if (p.grasped) return TL_INF_GRASPED_AGAIN;
+      if (k == TL_PICK && p.force == 0) return TL_INF_PICK_GRASP_NO_FORCE;
+      p.grasped = 1;
+      return 0;
+    case TL_EV_DROPPED:
+      if (!p.grasped) return TL_INF_DROPPED_NOT_GRASPED;
+      p.grasped = 0;
+      p.force = 0.0;
+      return 0;
+    case TL_EV_OBJ_AT_GOAL:
+    case TL_EV_OBJ_LEFT_GOAL:
+      draw = 1;
+      return 0;
+    case TL_EV_RELEASED_AT_GOAL:
+      if (!p.grasped) return TL_INF_RAG;
+      p.grasped = 0;
+      return 0;
+    case TL_EV_RELEASED_OUTSIDE_GOAL:
+      if (!p.grasped) return TL_INF_ROG;
+      p.grasped = 0;
+      return 0;
+    case TL_EV_SLIGHTLY_OPENED:
+      if (k != TL_OPEN || p.level != TL_LVL_LOW) return TL_INF_SLIGHTLY_OPENED;
+      p.level = TL_LVL_SLIGHT;
+      p.art = z.lv_slight;
+      return 0;
+    case TL_EV_OPENED:
+      if (k != TL_OPEN || p.level != TL_LVL_SLIGHT) return TL_INF_OPENED;
+      p.level = TL_LVL_OPEN;
+      p.art = z.lv_open;
+      return 0;
+    case TL_EV_CLOSED:
+      if (k == TL_OPEN) {
+        if (p.level != TL_LVL_OPEN) return TL_INF_CLOSED_OPEN;
+        p.level = TL_LVL_LOW;
+        p.art = z.lv_low;
+        return 0;
+      }
+      if (p.level != TL_LVL_SLIGHT) return TL_INF_CLOSED_CLOSE;
+      p.level = TL_LVL_CLOSED;
+      p.art = z.qmin;
+      return 0;
+    case TL_EV_SLIGHTLY_CLOSED:
+      if (p.level != TL_LVL_OPEN) return TL_INF_SC_LEVEL;
+      if (!z.band_valid) return TL_INF_SC_BAND;
+      p.level = TL_LVL_SLIGHT;
+      p.art = z.sc_art;
+      return 0;
+    case TL_EV_OPEN:
+      if (p.level != TL_LVL_CLOSED) return TL_INF_OPEN_CLOSE;
+      p.level = TL_LVL_OPEN;
+      p.art = z.a_q0 > z.closed_thresh ? z.a_q0 : z.qmax;
+      return 0;
+  }
+  return TL_INF_NOT_IN_ALPHABET;
+}
+
+__device__ __forceinline__ StepSt make_st(const RzConst& z, const PlanSt& p, int last_draw) {
+  StepSt s;
+  s.force = z.has_force ? __double2float_rn(p.force) : __int_as_float(0x7fc00000);
+  s.art = z.has_art ? __double2float_rn(p.art) : __int_as_float(0x7fc00000);
+  s.grasped = (uint8_t)p.grasped;
+  s.at_rest = (uint8_t)p.at_rest;
+  s.exc = (uint8_t)p.exc;
+  s.level = (uint8_t)p.level;
+  s.last_draw = (int16_t)last_draw;
+  s.pad = 0;
+  return s;
+}
+
+template <bool FUZZ, int DOFMAX>
+__global__ void __launch_bounds__(kSynthWarps * 32)
+    k_synth(SynthParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  SynthWarp& S = reinterpret_cast<SynthWarp*>(smem_raw)[warp];
+  const int dof = p.out.dof;
+  float* __restrict__ P = reinterpret_cast<float*>(p.out.planes);
+  const int64_t stride = p.out.plane_stride;
+  const float fnan = __int_as_float(0x7fc00000);
+
+  for (int e = blockIdx.x * kSynthWarps + warp; e < p.n_env; e += gridDim.x * kSynthWarps) {
+    // ---------------- reset: seed, (sample script), realizer constants -------
+    tl_script sc;
+    int64_t rs;
+    int n_rec = 0;
+    if (FUZZ) {
+      const int64_t seed = p.seeds[e];
+      if (lane < 2) mt_seed_lane(lane == 0 ? S.ring : S.mt, lane == 0 ? seed : (seed ^ 0x5EED));
+      __syncwarp();
+      mt_twist_warp(S.ring, nullptr, 0, 0);  // script RNG: first block
+      if (lane == 0) {
+        MtLane R{S.ring, 0};
+        tl_script t;
+        const int ns = sample_script(R, p.fuzz_subtask, p.cfg, S.kind, S.gap, t);
+        t.step_off = (int64_t)e * (p.cfg.max_events + 4);
+        t.seed = seed ^ 0x5EED;
+        int64_t nr = 1;
+        for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += S.gap[i];
+        const int64_t tmin = ns > 0 ? 0 : 1;
+        nr += t.tail > tmin ? t.tail : tmin;
+        if (nr < 2) nr = 2;
+        S.misc[0] = ns;
+        S.misc[1] = (ns < 0 || nr > p.cap_per_env) ? 1 : 0;
+        S.misc[2] = (int)nr;
+        S.misc[3] = t.tail;
+        S.misc[4] = t.initial_grasped;
+        S.misc[5] = t.initial_contact;
+        S.misc[6] = t.initial_level;
+        S.misc[7] = t.art_kind;
+        reinterpret_cast<double*>(&S.misc[8])[0] = t.initial_dist_obj_goal;
+        if (p.scripts_out) p.scripts_out[e] = t;
+        if (p.script_kind && ns > 0) {
+          for (int i = 0; i < ns; i++) {
+            p.script_kind[t.step_off + i] = S.kind[i];
+            p.script_gap[t.step_off + i] = S.gap[i];
+          }
+        }
+      }
+      __syncwarp();
+      sc.step_off = 0;
+      sc.seed = seed ^ 0x5EED;
+      sc.n_steps = S.misc[0];
+      sc.tail = S.misc[3];
+      sc.subtask = p.fuzz_subtask;
+      sc.art_kind = S.misc[7];
+      sc.initial_level = S.misc[6];
+      sc.initial_grasped = S.misc[4];
+      sc.initial_contact = S.misc[5];
+      sc.arm_dof = dof;
+      sc.initial_dist_obj_goal = reinterpret_cast<const double*>(&S.misc[8])[0];
+      rs = (int64_t)e * p.cap_per_env;
+      n_rec = S.misc[2];
+      const bool bad = S.misc[1] != 0;
+      __syncwarp();
+      if (lane == 0) {
+        p.out.rec_start[e] = rs;
+        p.out.n_rec[e] = bad ? 0 : n_rec;
+      }
+      if (bad) {
+        if (lane == 0) {
+          tl_label L;
+          L.status = TL_ERR_SCRIPT_CAPACITY; L.n_events = 0; L.err_index = -1;
+          L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
+          L.d0 = __longlong_as_double(0x7ff8000000000000ll);
+          p.labels[e] = L;
+        }
+        continue;
+      }
+    } else {
+      sc = p.scripts[e];
+      rs = p.out.rec_start[e];
+      n_rec = p.out.n_rec[e];
+      if (lane == 0) mt_seed_lane(S.mt, sc.seed);
+      __syncwarp();
+    }
+    const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
+    stage_cset(&S.cs, &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
+    RzConst z;
+    int st0 = realizer_init(z, sc, p.th, dof);
+    auto fail = [&](int code, int step) {
+      if (lane == 0) {
+        tl_label L;
+        L.status = code; L.n_events = 0; L.err_index = step;
+        L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
+        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
+        p.labels[e] = L;
+        if (FUZZ) p.out.n_rec[e] = 0;
+      }
+    };
+    if (st0 != TL_OK) { fail(st0, -1); continue; }
+
+    // initial realizer state (synth.py:111-158)
+    PlanSt ps;
+    ps.force = (z.has_force && sc.initial_contact) ? 1.2 : 0.0;
+    ps.grasped = sc.initial_grasped ? 1 : 0;
+    ps.at_rest = 0;
+    ps.exc = 0;
+    if (z.kind == TL_OPEN) {
+      ps.level = sc.initial_level;
+      ps.art = sc.initial_level == TL_LVL_LOW ? z.lv_low : sc.initial_level == TL_LVL_SLIGHT ? z.lv_slight : z.lv_open;
+    } else if (z.kind == TL_CLOSE) {
+      ps.level = sc.initial_level == TL_LVL_CLOSED ? TL_LVL_CLOSED : TL_LVL_OPEN;
+      ps.art = z.a_q0;
+    } else {
+      ps.level = TL_LVL_LOW;
+      ps.art = 0.0;
+    }
+    const double dist0 = z.has_goal ? sc.initial_dist_obj_goal : __longlong_as_double(0x7ff8000000000000ll);
+    const tl_cset& c = S.cs;
+    float sc_ru = 0.f;
+    double sc_d = 0.0;
+    if (c.subtask == TL_CLOSE) close_cut(c, (double)__double2float_rn(ps.art), sc_ru, sc_d);
+    const double d0 = (double)__double2float_rn(dist0);
+
+    // --------------- step windows -------------------------------------------
+    LState LS;
+    lstate_init(LS);
+    double cum = 0.0;            // lane 0 owns the serial f64 recurrence
+    double dist_carry = dist0;   // dist before the window
+    int32_t w_carry = 2 * z.ne;  // record 0 emits 2*dof+5 draws
+    int32_t tau_prev = 0;
+    uint32_t produced = 0;
+    int err_code = 0, err_step = -1;
+    int s_base = 0;
+    const int n_steps = sc.n_steps;
+    PlanSt pcarry = ps;
+    bool first_window = true;
+    for (;;) {
+      const int ns = min(n_steps - s_base, kMaxSteps);
+      const bool last_window = s_base + ns >= n_steps;
+      if (!FUZZ) {
+        for (int i = lane; i < ns; i += 32) {
+          S.kind[i] = p.step_kind[sc.step_off + s_base + i];
+          S.gap[i] = p.step_gap[sc.step_off + s_base + i];
+        }
+        __syncwarp();
+      }
+      // ---- plan (lane 0): record/word layout + deterministic state ------------
+      if (lane == 0) {
+        PlanSt q = pcarry;
+        int32_t w = w_carry, r = tau_prev;
+        int last_draw = -1, perr = 0, pstep = ns;
+        S.st[0] = make_st(z, q, -1);
+        for (int s = 0; s < ns; s++) {
+          const int g = S.gap[s];
+          if (g < 1) { perr = TL_INF_GAP; pstep = s; S.W[s] = w; S.hw[s] = 0; S.tau[s] = r; break; }
+          S.W[s] = w;
+          const int hwv = (q.exc ? 0 : 2) + (q.at_rest ? 0 : 2 * z.ne);
+          S.hw[s] = hwv;
+          w += (g - 1) * hwv;
+          r += g;
+          S.tau[s] = r;
+          int wev = q.exc ? 0 : 2;
+          int draw = 0;
+          const int ec = plan_apply(z, q, S.kind[s], draw);
+          S.sflag[s] = (uint8_t)draw;
+          if (ec) { perr = ec; pstep = s; break; }
+          if (draw) last_draw = s;
+          wev += (draw ? 2 : 0) + (q.at_rest ? 0 : 2 * z.ne);
+          w += wev;
+          S.st[s + 1] = make_st(z, q, last_draw);
+        }
+        if (!perr) {
+          S.W[ns] = w;
+          S.hw[ns] = (q.exc ? 0 : 2) + (q.at_rest ? 0 : 2 * z.ne);
+        }
+        S.misc[0] = perr;
+        S.misc[1] = pstep;
+        S.misc[2] = w;
+        S.misc[3] = r;
+        // carry for the next window
+        S.misc[4] = q.grasped; S.misc[5] = q.at_rest; S.misc[6] = q.exc; S.misc[7] = q.level;
+        reinterpret_cast<double*>(&S.misc[8])[0] = q.force;
+        reinterpret_cast<double*>(&S.misc[10])[0] = q.art;
+      }
+      __syncwarp();
+      const int perr = S.misc[0], pstep = S.misc[1];
+      // records of this window: (tau_prev, last event] or up to n_rec
+      const int r_begin = first_window ? 0 : tau_prev + 1;
+      int r_end;
+      if (perr) r_end = S.tau[pstep] + 1;
+      else if (last_window) r_end = n_rec;
+      else r_end = S.misc[3] + 1;
+      // ---- chunks of 32 records -----------------------------------------------
+      int seg_hint = 0;
+      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += 32) {
+        const int r = r0 + lane;
+        const bool valid = r < r_end;
+        int o = 0, adv = 0, app = 0, emit = 0, sidx = 0, ev = -1, s = 0;
+        if (valid) {
+          if (r == 0) {
+            emit = 1;  // initial record: no advance/apply, at_rest = False
+          } else {
+            s = seg_hint;
+            while (s < ns && S.tau[s] < r) s++;
+            if (s < ns && S.tau[s] == r) {
+              o = S.W[s] + (S.gap[s] - 1) * S.hw[s];
+              adv = !S.st[s].exc;
+              ev = S.kind[s];
+              app = (s < pstep || !perr) ? (S.sflag[s] & 1) : 0;
+              emit = (perr && s == pstep) ? 0 : !S.st[s + 1].at_rest;
+              sidx = (perr && s == pstep) ? s : s + 1;
+            } else {
+              const int first = (s == 0 ? tau_prev : S.tau[s - 1]) + 1;
+              o = S.W[s] + (r - first) * S.hw[s];
+              adv = !S.st[s].exc;
+              emit = !S.st[s].at_rest;
+              sidx = s;
+            }
+          }
+        }
+        seg_hint = __shfl_sync(kFull, s, 0);
+        // words needed by this chunk
+        const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
+        const int need_max = __reduce_max_sync(kFull, need);
+        while ((int)produced < need_max) {
+          mt_twist_warp(S.mt, S.ring, produced, kRingMask);
+          produced += kMtN;
+        }
+        const uint2* ring2 = reinterpret_cast<const uint2*>(S.ring);
+        auto rnd = [&](int woff) {
+          const uint2 wv = ring2[((uint32_t)woff & kRingMask) >> 1];
+          return rand53(wv.x, wv.y);
+        };
+        // advance_cum draw, object-distance draw and its feasibility check
+        int my_err = 0;
+        if (valid) {
+          S.radv[lane] = adv ? rnd(o) : -1.0;
+          S.rflag[lane] = (uint8_t)((adv ? 1 : 0) | (ev == TL_EV_EXCESSIVE_COLLISIONS && !(perr && s == pstep) ? 2 : 0));
+          if (app) {
+            const double rr = rnd(o + 2 * adv);
+            S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rr) : uniform_rn(0.3, 0.8, rr);
+          }
+        }
+        __syncwarp();
+        double dist_rec = dist_carry;
+        if (valid && z.has_goal) {
+          const int ld = S.st[sidx].last_draw;
+          dist_rec = ld >= 0 ? S.dist_after[ld] : dist_carry;
+          if (ev >= 0) {
+            const int ldb = S.st[s].last_draw;
+            const double db = ldb >= 0 ? S.dist_after[ldb] : dist_carry;
+            switch (ev) {  // value-dependent checks of _apply (synth.py:218-260)
+              case TL_EV_OBJ_AT_GOAL: if (db <= z.goal) my_err = TL_INF_AT_GOAL_ALREADY; break;
+              case TL_EV_OBJ_LEFT_GOAL: if (db > z.goal) my_err = TL_INF_LEFT_NOT_AT_GOAL; break;
+              case TL_EV_RELEASED_AT_GOAL: if (db > z.goal) my_err = TL_INF_RAG; break;
+              case TL_EV_RELEASED_OUTSIDE_GOAL: if (db <= z.goal) my_err = TL_INF_ROG; break;
+              case TL_EV_SUCCESS: if (db > z.goal) my_err = TL_INF_SUCCESS_UNREACHABLE; break;
+            }
+          }
+        }
+        if (valid && perr && ev >= 0 && s == pstep && !my_err) my_err = perr;
+        const unsigned eb = __ballot_sync(kFull, my_err != 0);
+        if (eb) {
+          const int L = __ffs(eb) - 1;
+          err_code = __shfl_sync(kFull, my_err, L);
+          err_step = s_base + __shfl_sync(kFull, s, L);
+          break;
+        }
+        // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213)
+        const int cnt = min(32, r_end - r0);
+        if (lane == 0) {
+          for (int j = 0; j < cnt; j++) {
+            const uint8_t f = S.rflag[j];
+            if (f & 1) {
+              const double h = __dsub_rn(z.L09, cum);
+              cum = __dadd_rn(cum, uniform_rn(0.0, __dmul_rn(h, 0.05), S.radv[j]));
+            }
+            if (f & 2) cum = z.L105;
+            S.cum32[j] = __double2float_rn(cum);
+          }
+        }
+        __syncwarp();
+        // ---- emit + write + label ---------------------------------------------
+        RecV<float> v;
+        uint32_t ind = 0, errb = 0;
+        if (valid) {
+          const int64_t rr = rs + r;
+          const StepSt stv = S.st[sidx];
+          const int eo = o + 2 * adv + 2 * app;
+          float mq = 0.f, mqd = 0.f;
+#pragma unroll
+          for (int i = 0; i < DOFMAX; i++) {
+            if (i < dof) {
+              const float q = emit ? __double2float_rn(uniform_rn(-0.3, 0.3, rnd(eo + 2 * i))) : 0.f;
+              P[i * stride + rr] = q;
+              mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < DOFMAX; i++) {
+            if (i < dof) {
+              const float qd = emit ? __double2float_rn(uniform_rn(-0.4, 0.4, rnd(eo + 2 * (dof + i)))) : 0.f;
+              P[(dof + i) * stride + rr] = qd;
+              mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
+            }
+          }
+          const int eb2 = eo + 4 * dof;
+          v.tor = emit ? __double2float_rn(uniform_rn(-0.05, 0.05, rnd(eb2))) : 0.f;
+          v.vx = emit ? __double2float_rn(uniform_rn(-0.2, 0.2, rnd(eb2 + 2))) : 0.f;
+          v.vy = emit ? __double2float_rn(uniform_rn(-0.2, 0.2, rnd(eb2 + 4))) : 0.f;
+          v.om = emit ? __double2float_rn(uniform_rn(-0.3, 0.3, rnd(eb2 + 6))) : 0.f;
+          v.der = emit ? __double2float_rn(uniform_rn(0.2, 1.0, rnd(eb2 + 8))) : 0.f;
+          v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
+          v.force = stv.force;
+          v.cum = S.cum32[lane];
+          v.art = stv.art;
+          v.g = stv.grasped != 0;
+          v.qdm = mqd;
+          v.jm = mq;
+          v.jm_d = 0.0;
+          const int f0 = 2 * dof;
+          P[f0 * stride + rr] = v.tor;
+          P[(f0 + 1) * stride + rr] = v.vx;
+          P[(f0 + 2) * stride + rr] = v.vy;
+          P[(f0 + 3) * stride + rr] = v.om;
+          P[(f0 + 4) * stride + rr] = v.der;
+          P[(f0 + 5) * stride + rr] = v.dist;
+          P[(f0 + 6) * stride + rr] = v.force;
+          P[(f0 + 7) * stride + rr] = v.cum;
+          P[(f0 + 8) * stride + rr] = v.art;
+          p.out.grasped[rr] = (uint8_t)v.g;
+          record_bits(c, v, sc_ru, sc_d, ind, errb);
+        }
+        uint32_t prev = __shfl_up_sync(kFull, ind, 1);
+        if (lane == 0) prev = LS.prev_ind;
+        const uint32_t mask = (valid && r > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
+        if (valid && p.step_mask) p.step_mask[rs + r] = (uint8_t)mask;
+        lstate_fold(LS, mask, valid ? errb : 0u);
+        const int lastl = cnt - 1;
+        LS.prev_ind = __shfl_sync(kFull, ind, lastl);
+      }
+      // a plan error whose step has no event record of its own (gap < 1)
+      if (!err_code && perr) { err_code = perr; err_step = s_base + pstep; }
+      if (err_code || last_window) break;
+      // object distance carried into the next window
+      {
+        const int ld = S.st[ns].last_draw;
+        if (ld >= 0) dist_carry = S.dist_after[ld];
+      }
+      // next window
+      pcarry.grasped = S.misc[4]; pcarry.at_rest = S.misc[5]; pcarry.exc = S.misc[6]; pcarry.level = S.misc[7];
+      pcarry.force = reinterpret_cast<const double*>(&S.misc[8])[0];
+      pcarry.art = reinterpret_cast<const double*>(&S.misc[10])[0];
+      w_carry = S.misc[2];
+      tau_prev = S.misc[3];
+      s_base += ns;
+      first_window = false;
+      __syncwarp();
+    }
+    if (err_code) { fail(err_code, err_step); continue; }
+    finish_label(c, LS, d0, p.rules, &p.labels[e]);
+    __syncwarp();
+  }
+}
+
+}  // namespace tl

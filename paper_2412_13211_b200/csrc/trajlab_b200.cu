@@ -1,0 +1,386 @@
+// trajlab_b200.cu -- C ABI of libtrajlab_b200.so (see include/trajlab_b200.h).
+// Single translation unit: kernels live in the tl_*.cuh headers.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "tl_common.cuh"
+#include "tl_label.cuh"
+#include "tl_synth.cuh"
+#include "tl_filter.cuh"
+
+namespace {
+
+using namespace tl;
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "trajlab_b200: CUDA error: %s\n", cudaGetErrorString(e));
+    return TL_E_CUDA;
+  }
+  return TL_OK;
+}
+
+int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// default rule tables = MODE_RULES (modes.py:208-213): success rules then
+// failure rules of each subtask, in declaration order
+tl_rules default_rules() {
+  static const int base[4] = {0, 9, 21, 30}, ns[4] = {4, 5, 3, 3}, nm[4] = {9, 12, 9, 9};
+  tl_rules r;
+  memset(&r, 0, sizeof(r));
+  for (int s = 0; s < 4; s++) {
+    r.count[s][0] = (int8_t)ns[s];
+    for (int i = 0; i < ns[s]; i++) r.ids[s][0][i] = (int8_t)(base[s] + i);
+    r.count[s][1] = (int8_t)(nm[s] - ns[s]);
+    for (int i = ns[s]; i < nm[s]; i++) r.ids[s][1][i - ns[s]] = (int8_t)(base[s] + i);
+  }
+  return r;
+}
+
+tl_rules rules_or_default(const tl_rules* r) { return r ? *r : default_rules(); }
+
+// largest float <= x / smallest float >= x (x finite or inf; NaN stays NaN)
+float rd_f32(double x) {
+  float f = (float)x;
+  if (std::isnan(x)) return f;
+  if ((double)f > x) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+float ru_f32(double x) {
+  float f = (float)x;
+  if (std::isnan(x)) return f;
+  if ((double)f < x) f = std::nextafter(f, INFINITY);
+  return f;
+}
+
+template <class F>
+void set_max_smem(F* k, int bytes) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int blocks_for(int n_items, int per_block, int max_blocks) {
+  int b = (n_items + per_block - 1) / per_block;
+  if (b > max_blocks) b = max_blocks;
+  return b < 1 ? 1 : b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tl_abi_version(void) { return TL_ABI_VERSION; }
+
+int tl_device_sm_count(void) { return sm_count(); }
+
+const char* tl_status_name(int code) {
+  switch (code) {
+    case TL_OK: return "OK";
+    case TL_ERR_TOO_SHORT: return "TooShort";
+    case TL_ERR_NAN_SUCCESS_DIST: case TL_ERR_NAN_ART: case TL_ERR_NAN_FORCE:
+    case TL_ERR_NAN_PLACE_DIST: return "RequiredFieldNaN";
+    case TL_ERR_MISSING_ART: return "MissingArticulation";
+    case TL_ERR_MODE_COVERAGE: return "ModeCoverageError";
+    case TL_ERR_D0_NONE_LE: case TL_ERR_D0_NONE_GT: return "TypeError";
+    case TL_ERR_SCRIPT_CAPACITY: return "ScriptCapacity";
+    case TL_E_INVALID: return "InvalidArgument";
+    case TL_E_CUDA: return "CudaError";
+    case TL_E_CAPACITY: return "Capacity";
+    default:
+      if (code >= TL_INF_PICK_GRASPED_NO_CONTACT && code <= TL_INF_INIT_LEVEL) return "InfeasibleScript";
+      return "Unknown";
+  }
+}
+
+// TrajectoryHeader + Thresholds -> cset (predicates.py:43-94 thresholds,
+// thresholds.py:44-60 lookups).  All f64 arithmetic in the reference order.
+int tl_cset_build(int32_t subtask, int32_t art_kind, double art_qmin, double art_qmax,
+                  int32_t arm_dof, const double* rest_arm, double rest_tor,
+                  const tl_thresholds* th, tl_cset* out) {
+  if (!th || !out || subtask < 0 || subtask > 3 || arm_dof < 1 || arm_dof > TL_MAX_DOF ||
+      art_kind < 0 || art_kind > 2)
+    return TL_E_INVALID;
+  tl_cset c;
+  memset(&c, 0, sizeof(c));
+  c.subtask = subtask;
+  c.art_kind = art_kind;
+  c.dof = arm_dof;
+  int zero = rest_tor == 0.0;
+  for (int i = 0; i < arm_dof; i++) {
+    c.rest_arm[i] = rest_arm ? rest_arm[i] : 0.0;
+    if (c.rest_arm[i] != 0.0) zero = 0;
+  }
+  c.rest_zero = zero;
+  c.rest_tor = rest_tor;
+  const double limit = subtask == TL_PICK ? th->coll_pick : subtask == TL_PLACE ? th->coll_place : th->coll_artic;
+  const double span = art_qmax - art_qmin;  // (qmax - qmin)
+  const double ofrac = art_kind == TL_ART_FRIDGE ? th->open_frac_fridge : th->open_frac_drawer;
+  volatile double t;  // keep each product rounded before the add (no FMA)
+  t = ofrac * span;
+  c.open_cut = t + art_qmin;
+  t = th->close_frac * span;
+  c.closed_cut = t + art_qmin;
+  t = th->slightly_open_frac * span;
+  c.slight_open_cut = t + art_qmin;
+  t = th->slightly_close_frac * span;
+  c.scf_span = t;
+  c.rest_radius = th->rest_radius;
+  c.goal_radius = th->goal_radius;
+  c.static_qd = th->static_qd_arm;
+  c.static_v = th->static_v_base;
+  c.static_om = th->static_omega;
+  c.limit = limit;
+  c.contact_eps = th->contact_eps;
+  c.j_arm = subtask == TL_PICK ? th->j_arm_pick : th->j_arm_other;
+  c.j_tor = th->j_tor_max;
+  c.rd_rest_radius = rd_f32(c.rest_radius);
+  c.rd_goal = rd_f32(c.goal_radius);
+  c.rd_static_qd = rd_f32(c.static_qd);
+  c.rd_static_v = rd_f32(c.static_v);
+  c.rd_static_om = rd_f32(c.static_om);
+  c.rd_limit = rd_f32(limit);
+  c.rd_contact = rd_f32(c.contact_eps);
+  c.ru_open = ru_f32(c.open_cut);
+  c.rd_closed = rd_f32(c.closed_cut);
+  c.ru_slight_open = ru_f32(c.slight_open_cut);
+  c.rd_j_arm = rd_f32(c.j_arm);
+  c.rd_j_tor = rd_f32(c.j_tor);
+  *out = c;
+  return TL_OK;
+}
+
+int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_cset,
+                     const tl_cset* csets, int32_t n_cset, const tl_rules* rules,
+                     uint8_t* step_mask, uint8_t* step_success, tl_label* labels,
+                     void* stream) {
+  if (!recs || !labels || !env_cset || !csets || n_env < 0 || n_cset < 1 || recs->dof < 1 ||
+      recs->dof > TL_MAX_DOF || (recs->dtype != 0 && recs->dtype != 1))
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  const tl_rules r = rules_or_default(rules);
+  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * 16);
+  const dim3 blk(kLabelWarps * 32);
+  const bool small = recs->dof <= 7;
+  if (recs->dtype == 0) {
+    if (small) k_label<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
+    else k_label<float, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
+  } else {
+    if (small) k_label<double, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
+    else k_label<double, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
+  }
+  return check_launch();
+}
+
+size_t tl_scan_scratch_bytes(int32_t n) {
+  const size_t tiles = ((size_t)(n > 0 ? n : 1) + kScanBlock - 1) / kScanBlock;
+  return tiles * sizeof(int64_t);
+}
+
+int tl_scan_events(const tl_label* labels, int32_t n, int64_t* ev_off, void* scratch, void* stream) {
+  if (!ev_off || n < 0 || (n > 0 && (!labels || !scratch))) return TL_E_INVALID;
+  if (n == 0) {
+    cudaMemsetAsync(ev_off, 0, sizeof(int64_t), S(stream));
+    return check_launch();
+  }
+  const int tiles = (n + kScanBlock - 1) / kScanBlock;
+  int64_t* tile = reinterpret_cast<int64_t*>(scratch);
+  k_scan_tiles<<<tiles, kScanBlock, 0, S(stream)>>>(labels, n, ev_off, tile);
+  k_scan_sums<<<1, kScanBlock, 0, S(stream)>>>(tile, tiles, ev_off, n);
+  k_scan_add<<<(n + 255) / 256, 256, 0, S(stream)>>>(ev_off, tile, n);
+  return check_launch();
+}
+
+int tl_emit_events(const uint8_t* step_mask, const int64_t* rec_start, const int32_t* n_rec,
+                   const tl_label* labels, const int64_t* ev_off, int32_t n_env, uint8_t* ev_kind,
+                   int32_t* ev_t, void* stream) {
+  if (n_env < 0 || (n_env > 0 && (!step_mask || !rec_start || !n_rec || !labels || !ev_off ||
+                                  !ev_kind || !ev_t)))
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  const int grid = blocks_for(n_env, kEmitWarps, sm_count() * 16);
+  k_emit<<<grid, kEmitWarps * 32, 0, S(stream)>>>(step_mask, rec_start, n_rec, labels, ev_off, n_env, ev_kind, ev_t);
+  return check_launch();
+}
+
+int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint8_t* subtask,
+                       const double* d0, const uint8_t* d0_none, int32_t n, const tl_rules* rules,
+                       tl_label* out, void* stream) {
+  if (n < 0 || (n > 0 && (!ev_off || !subtask || !out))) return TL_E_INVALID;
+  if (n == 0) return TL_OK;
+  const tl_rules r = rules_or_default(rules);
+  k_classify_events<<<(n + 127) / 128, 128, 0, S(stream)>>>(ev_kind, ev_off, subtask, d0, d0_none, n, r, out);
+  return check_launch();
+}
+
+static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
+  const int smem = kSynthWarps * (int)sizeof(SynthWarp);
+  const bool small = sp.out.dof <= 7;
+  void (*k)(SynthParams) = fuzz ? (small ? k_synth<true, 7> : k_synth<true, 16>)
+                                : (small ? k_synth<false, 7> : k_synth<false, 16>);
+  set_max_smem(k, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSynthWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int grid = blocks_for(sp.n_env, kSynthWarps, sm_count() * per_sm);
+  k<<<grid, kSynthWarps * 32, smem, S(stream)>>>(sp);
+  return check_launch();
+}
+
+int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
+            const tl_thresholds* th_realize, const tl_cset* label_csets, const tl_rules* rules,
+            tl_records* out, int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
+            tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* stream) {
+  if (!cfg || !th_realize || !label_csets || !out || !labels || n_env < 0 || subtask < 0 ||
+      subtask > 3 || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
+      cfg->max_gap < 1 || cfg->max_tail < 1 || cfg->max_events < 0 ||
+      cfg->max_events + 4 > kMaxSteps || cap_per_env < 2 || (script_kind && !script_gap))
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  SynthParams sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.seeds = seeds;
+  sp.fuzz_subtask = subtask;
+  sp.cfg = *cfg;
+  sp.script_kind = script_kind;
+  sp.script_gap = script_gap;
+  sp.scripts_out = scripts;
+  sp.n_env = n_env;
+  sp.cap_per_env = cap_per_env;
+  sp.th = *th_realize;
+  sp.label_csets = label_csets;
+  sp.rules = rules_or_default(rules);
+  sp.out = *out;
+  sp.step_mask = step_mask;
+  sp.labels = labels;
+  return launch_synth(sp, true, stream);
+}
+
+int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t* step_gap,
+               int32_t n_env, const tl_thresholds* th_realize, const tl_cset* label_csets,
+               const tl_rules* rules, tl_records* out, uint8_t* step_mask, tl_label* labels,
+               void* stream) {
+  if (!scripts || !th_realize || !label_csets || !out || !labels || n_env < 0 ||
+      out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF)
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  SynthParams sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.scripts = scripts;
+  sp.step_kind = step_kind;
+  sp.step_gap = step_gap;
+  sp.n_env = n_env;
+  sp.th = *th_realize;
+  sp.label_csets = label_csets;
+  sp.rules = rules_or_default(rules);
+  sp.out = *out;
+  sp.step_mask = step_mask;
+  sp.labels = labels;
+  return launch_synth(sp, false, stream);
+}
+
+size_t tl_filter_scratch_bytes(int64_t n, int32_t n_buckets, int32_t n_pools) {
+  const int64_t tiles = (n + kFilterTile - 1) / kFilterTile;
+  const size_t a = (size_t)(tiles > 0 ? tiles : 1) * (size_t)(n_buckets > 0 ? n_buckets : 1) * 4;
+  const size_t a8 = (a + 15) & ~(size_t)15;
+  return a8 + 2 * (size_t)(n_buckets > 0 ? n_buckets : 1) * 8 + (size_t)(n_pools + 1) * 0;
+}
+
+int tl_filter_select(const int32_t* bucket, int64_t n, int32_t n_buckets, int32_t n_pools,
+                     const int32_t* pool_b0, const double* bucket_w, int64_t quota,
+                     uint8_t* selected, int64_t* pool_selected, void* scratch, void* stream) {
+  if (n < 0 || n_buckets < 0 || n_pools < 0 || quota < 0 || !scratch ||
+      (n > 0 && (!bucket || !selected)) || (n_pools > 0 && (!pool_b0 || !pool_selected)))
+    return TL_E_INVALID;
+  if (n_buckets * 4 > 200 * 1024) return TL_E_CAPACITY;
+  const int64_t tiles = (n + kFilterTile - 1) / kFilterTile;
+  int32_t* tile_cnt = reinterpret_cast<int32_t*>(scratch);
+  const size_t a = (size_t)(tiles > 0 ? tiles : 1) * (size_t)(n_buckets > 0 ? n_buckets : 1) * 4;
+  int64_t* cnt = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scratch) + ((a + 15) & ~(size_t)15));
+  int64_t* take = cnt + (n_buckets > 0 ? n_buckets : 1);
+  const int hsmem = n_buckets * 4;
+  if (hsmem > 48 * 1024) {
+    set_max_smem(k_filter_hist, hsmem);
+    set_max_smem(k_filter_select, hsmem);
+  }
+  if (n_buckets > 0) {
+    if (tiles > 0) k_filter_hist<<<(unsigned)tiles, 256, hsmem, S(stream)>>>(bucket, n, n_buckets, tile_cnt);
+    else cudaMemsetAsync(tile_cnt, 0, (size_t)n_buckets * 4, S(stream));
+    k_filter_colscan<<<(n_buckets + 127) / 128, 128, 0, S(stream)>>>(tile_cnt, (int)tiles, n_buckets, cnt);
+  }
+  if (n_pools > 0)
+    k_filter_pool<<<(n_pools + 127) / 128, 128, 0, S(stream)>>>(pool_b0, n_pools, bucket_w, cnt, quota, take, pool_selected);
+  if (tiles > 0) {
+    if (n_buckets > 0)
+      k_filter_select<<<(unsigned)tiles, 32, hsmem, S(stream)>>>(bucket, n, n_buckets, tile_cnt, take, selected);
+    else
+      cudaMemsetAsync(selected, 0, (size_t)n, S(stream));
+  }
+  return check_launch();
+}
+
+int tl_eval_predicates(const tl_records* recs, int32_t n_env, const int32_t* env_cset,
+                       const tl_cset* csets, const double* a0, uint8_t* bits, uint8_t* errs,
+                       double* jmax, void* stream) {
+  if (!recs || !env_cset || !csets || n_env < 0 || recs->dof < 1 || recs->dof > TL_MAX_DOF ||
+      (recs->dtype != 0 && recs->dtype != 1))
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * 16);
+  const dim3 blk(kLabelWarps * 32);
+  if (recs->dtype == 0) {
+    if (recs->dof <= 7) k_predicates<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, a0, bits, errs, jmax);
+    else k_predicates<float, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, a0, bits, errs, jmax);
+  } else {
+    if (recs->dof <= 7) k_predicates<double, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, a0, bits, errs, jmax);
+    else k_predicates<double, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, a0, bits, errs, jmax);
+  }
+  return check_launch();
+}
+
+int tl_scan_counts(const int32_t* counts, int32_t n, int64_t* off, void* scratch, void* stream) {
+  if (!off || n < 0 || (n > 0 && (!counts || !scratch))) return TL_E_INVALID;
+  if (n == 0) {
+    cudaMemsetAsync(off, 0, sizeof(int64_t), S(stream));
+    return check_launch();
+  }
+  const int tiles = (n + kScanBlock - 1) / kScanBlock;
+  int64_t* tile = reinterpret_cast<int64_t*>(scratch);
+  k_scan_i32_tiles<<<tiles, kScanBlock, 0, S(stream)>>>(counts, n, off, tile);
+  k_scan_sums<<<1, kScanBlock, 0, S(stream)>>>(tile, tiles, off, n);
+  k_scan_add<<<(n + 255) / 256, 256, 0, S(stream)>>>(off, tile, n);
+  return check_launch();
+}
+
+int tl_compact_records(const tl_records* src, int32_t n_env, const int64_t* dst_start,
+                       tl_records* dst, void* stream) {
+  if (!src || !dst || !dst_start || n_env < 0 || src->dtype != dst->dtype || src->dof != dst->dof)
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  const int np_ = 2 * src->dof + 9;
+  const int grid = blocks_for(n_env, 8, sm_count() * 8);
+  if (src->dtype == 0) k_compact<float><<<grid, 256, 0, S(stream)>>>(*src, n_env, dst_start, *dst, np_);
+  else k_compact<double><<<grid, 256, 0, S(stream)>>>(*src, n_env, dst_start, *dst, np_);
+  return check_launch();
+}
+
+int tl_mode_histogram(const tl_label* labels, int32_t n, int64_t* hist, void* stream) {
+  if (!hist || n < 0 || (n > 0 && !labels)) return TL_E_INVALID;
+  cudaMemsetAsync(hist, 0, TL_N_MODES * sizeof(int64_t), S(stream));
+  if (n > 0)
+    k_mode_hist<<<blocks_for(n, 256, sm_count() * 4), 256, 0, S(stream)>>>(
+        labels, n, reinterpret_cast<unsigned long long*>(hist));
+  return check_launch();
+}
+
+}  // extern "C"

@@ -1,0 +1,327 @@
+"""GPU parity: libtrajlab_b200.so (sm_100a) vs the reference's golden
+fixtures and vs the CPU oracle.  Integer / event / mode / record outputs
+must be bit-exact.  Runs on a B200 (-m gpu)."""
+import math
+
+import numpy as np
+import pytest
+
+from golden_data import (DOF, SUBTASKS, Corpus, fuzz_corpus, js, npz,
+                         same_bits_f32)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def C():
+    from paper_2412_13211_b200 import core
+    return core
+
+
+@pytest.fixture(scope="module")
+def TH():
+    from paper_2412_13211_b200.thresholds import Thresholds
+    return Thresholds
+
+
+def corpus_batch(C, TH, c: Corpus, dtype=np.float32, overrides=None):
+    """fixture corpus -> RecordBatch + csets (planes copied verbatim)."""
+    dev = torch.device("cuda")
+    planes = torch.from_numpy(np.ascontiguousarray(c.planes.astype(dtype))).to(dev)
+    if planes.shape[1] == 0:
+        planes = torch.zeros((planes.shape[0], 1), dtype=planes.dtype, device=dev)
+    g = torch.from_numpy(np.ascontiguousarray(c.grasped) if len(c.grasped) else np.zeros(1, np.uint8)).to(dev)
+    rs = torch.from_numpy(c.rec_off[:-1].copy()).to(dev)
+    nr = torch.from_numpy(np.diff(c.rec_off).astype(np.int32)).to(dev)
+    rb = C.RecordBatch(planes, g, rs, nr, DOF)
+    tab = C.CsetTable()
+    env = np.zeros(c.n, np.int32)
+    for i in range(c.n):
+        th = TH()
+        if overrides is not None and overrides[i] is not None:
+            th = TH(**overrides[i])
+        env[i] = tab.add(int(c.subtask[i]), int(c.art_kind[i]), float(c.art_qmin[i]),
+                         float(c.art_qmax[i]), DOF, list(c.rest_arm[i]),
+                         float(c.rest_tor[i]), th)
+    return rb, torch.from_numpy(env).to(dev), tab.to_device(dev), len(tab)
+
+
+def check_labels(res, c: Corpus, err_type=None):
+    lab = res.labels_np()
+    ev_off = res.ev_off.cpu().numpy()
+    ek = res.ev_kind.cpu().numpy()
+    et = res.ev_t.cpu().numpy()
+    from paper_2412_13211_b200 import _lib as L
+    for i in range(c.n):
+        if err_type is not None and err_type[i]:
+            assert lab["status"][i] != 0, i
+            name = L.lib().tl_status_name(int(lab["status"][i])).decode()
+            assert name == err_type[i], (i, name, err_type[i])
+            continue
+        assert lab["status"][i] == 0, (i, lab["status"][i])
+        want_k, want_t = c.events(i)
+        a, b = ev_off[i], ev_off[i + 1]
+        assert list(ek[a:b]) == want_k, i
+        assert list(et[a:b]) == want_t, i
+        assert lab["mode"][i] == c.mode[i], i
+        assert bool(lab["flags"][i] & 1) == bool(c.success_once[i])
+        assert bool(lab["flags"][i] & 2) == bool(c.success_at_end[i])
+        assert lab["n_events"][i] == len(want_k)
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_label_fuzz_fixtures(C, TH, kind):
+    c = fuzz_corpus(kind)
+    rb, env, cs, n = corpus_batch(C, TH, c)
+    res = C.label_records(rb, env, cs, n)
+    check_labels(res, c)
+
+
+def test_label_defining_and_long(C, TH):
+    for c in (Corpus(npz("defining")), Corpus(npz("long"))):
+        rb, env, cs, n = corpus_batch(C, TH, c)
+        check_labels(C.label_records(rb, env, cs, n), c)
+
+
+@pytest.mark.parametrize("tag,dtype", [("f32_", np.float32), ("f64_", np.float64)])
+def test_label_crafted(C, TH, tag, dtype):
+    d = npz("crafted")
+    c = Corpus(d, tag)
+    fields = list(d["threshold_fields"])
+    ov = [dict(zip(fields, map(float, d[tag + "override"][i]))) if d[tag + "has_override"][i] else None
+          for i in range(c.n)]
+    rb, env, cs, n = corpus_batch(C, TH, c, dtype, ov)
+    res = C.label_records(rb, env, cs, n, want_success=True)
+    check_labels(res, c, d[tag + "err_type"])
+    # per-record success_step (predicates.py:75-94), incl. raising records
+    got = res.step_success.cpu().numpy()[:c.rec_off[-1]]
+    assert np.array_equal(got, d[tag + "success_step"])
+
+
+def _fuzz_records(sb, e):
+    rs = int(sb.records.rec_start[e].item())
+    n = int(sb.records.n_rec[e].item())
+    return sb.records.planes[:, rs:rs + n].cpu().numpy(), sb.records.grasped[rs:rs + n].cpu().numpy()
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_fuzz_generation_matches_reference(C, TH, kind):
+    from paper_2412_13211_b200.synth import FuzzConfig
+    c = fuzz_corpus(kind)
+    seeds = npz("fuzz")["seeds"]
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    sb = C.fuzz_batch(seeds, kind, FuzzConfig(), TH(), cs, want_scripts=True)
+    torch.cuda.synchronize()
+    lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    scripts = c.scripts()
+    sk = sb.script_kind.cpu().numpy()
+    sg = sb.script_gap.cpu().numpy()
+    for i in range(len(seeds)):
+        planes, g = _fuzz_records(sb, i)
+        wp, wg = c.records_np(i)
+        assert same_bits_f32(planes, wp), (kind, int(seeds[i]))
+        assert np.array_equal(g, wg)
+        assert lab["status"][i] == 0
+        assert lab["mode"][i] == c.mode[i]
+        ns = len(scripts[i]["kinds"])
+        off = i * 12
+        assert list(sk[off:off + ns]) == list(scripts[i]["kinds"])
+        assert list(sg[off:off + ns]) == list(scripts[i]["gaps"])
+
+
+def test_fuzz_g64_matches_reference(C, TH):
+    from paper_2412_13211_b200.synth import FuzzConfig
+    d = npz("long")
+    cfg = FuzzConfig(max_gap=64, max_tail=64)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    for k, name in enumerate(("pick", "place", "open", "close")):
+        c = Corpus(d, "g64_" + name + "_")
+        sb = C.fuzz_batch(np.arange(16), k, cfg, TH(), cs)
+        for i in range(16):
+            planes, _ = _fuzz_records(sb, i)
+            assert same_bits_f32(planes, c.records_np(i)[0]), (name, i)
+
+
+def _scripts_np(C, scripts, seeds):
+    from paper_2412_13211_b200 import _lib as L
+    arr = np.zeros(len(scripts), L.SCRIPT_DTYPE)
+    kinds, gaps = [], []
+    for i, sc in enumerate(scripts):
+        arr[i]["step_off"] = len(kinds)
+        arr[i]["seed"] = int(seeds[i])
+        arr[i]["n_steps"] = len(sc["kinds"])
+        arr[i]["tail"] = sc["tail"]
+        arr[i]["subtask"] = sc["subtask"]
+        arr[i]["art_kind"] = sc["art_kind"]
+        arr[i]["initial_level"] = sc["initial_level"]
+        arr[i]["initial_grasped"] = sc["initial_grasped"]
+        arr[i]["initial_contact"] = sc["initial_contact"]
+        arr[i]["arm_dof"] = 7
+        arr[i]["initial_dist_obj_goal"] = sc["initial_dist_obj_goal"]
+        kinds.extend(int(k) for k in sc["kinds"])
+        gaps.extend(int(g) for g in sc["gaps"])
+    return arr, np.asarray(kinds, np.uint8), np.asarray(gaps, np.int32)
+
+
+def test_realize_defining_and_long(C, TH):
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    for d in (npz("defining"), npz("long")):
+        c = Corpus(d)
+        arr, k, g = _scripts_np(C, c.scripts(), d["seed"])
+        sb = C.realize_batch(arr, k, g, TH(), cs)
+        lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+        planes = sb.records.planes.cpu().numpy()
+        for i in range(c.n):
+            a, b = c.rec_off[i], c.rec_off[i + 1]
+            assert same_bits_f32(planes[:, a:b], c.planes[:, a:b]), i
+            assert lab["status"][i] == 0 and lab["mode"][i] == c.mode[i], i
+
+
+def test_realize_arbitrary_scripts(C, TH):
+    """scripts.json: feasible scripts realize bit-exactly, infeasible ones
+    report the reference's InfeasibleScript raise site and message."""
+    from paper_2412_13211_b200 import errors as ER
+    from golden_data import LEVELS, ART
+    EV = ("Contact", "Grasped", "Dropped", "ObjAtGoal", "ReleasedAtGoal",
+          "ReleasedOutsideGoal", "ObjLeftGoal", "Opened", "SlightlyOpened", "Closed",
+          "SlightlyClosed", "Open", "Success", "ExcessiveCollisions")
+    cases = js("scripts")
+    groups = {}
+    for case in cases:
+        key = json_key = str(case["thresholds"])
+        groups.setdefault(key, []).append(case)
+    for key, group in groups.items():
+        th = TH(**group[0]["thresholds"]) if group[0]["thresholds"] else TH()
+        scripts, seeds = [], []
+        for case in group:
+            scripts.append(dict(subtask=SUBTASKS.index(case["subtask"]),
+                                kinds=[EV.index(s[0]) for s in case["steps"]],
+                                gaps=[s[1] for s in case["steps"]], tail=case["tail"],
+                                initial_grasped=int(case["initial_grasped"]),
+                                initial_contact=int(case["initial_contact"]),
+                                initial_level=LEVELS.index(case["initial_art_level"]),
+                                art_kind=ART.index(case["articulation_kind"]),
+                                initial_dist_obj_goal=case["initial_dist_obj_goal"]))
+            seeds.append(case["seed"])
+        cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+        arr, k, g = _scripts_np(C, scripts, seeds)
+        sb = C.realize_batch(arr, k, g, th, cs)
+        lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+        planes = sb.records.planes.cpu().numpy()
+        rs = sb.records.rec_start.cpu().numpy()
+        nr = sb.records.n_rec.cpu().numpy()
+        for i, case in enumerate(group):
+            if case["error"] is not None:
+                st = int(lab["status"][i])
+                step = int(lab["err"][i])
+                ev = case["steps"][step][0] if step >= 0 else None
+                exc = ER.infeasible_error(st, case["subtask"], ev, case["initial_art_level"])
+                assert [type(exc).__name__, str(exc)] == case["error"], (case, st, step)
+                continue
+            assert lab["status"][i] == 0, (case, lab["status"][i])
+            n = case["n_records"]
+            assert nr[i] == n
+            p = planes[:, rs[i]:rs[i] + n]
+            vals = np.concatenate([p[:, t] for t in range(n)]) if n else np.zeros(0)
+            # fixture order per record: q_arm, qd_arm, 9 scalars, grasped
+            g_ = sb.records.grasped[rs[i]:rs[i] + n].cpu().numpy().astype(np.float32)
+            got = np.concatenate([np.concatenate([p[:, t], [g_[t]]]) for t in range(n)])
+            want = np.frombuffer(bytes.fromhex(case["records_f32_hex"]), np.float32)
+            assert same_bits_f32(got, want), case
+
+
+def test_classify_cases(C):
+    EV = ("Contact", "Grasped", "Dropped", "ObjAtGoal", "ReleasedAtGoal",
+          "ReleasedOutsideGoal", "ObjLeftGoal", "Opened", "SlightlyOpened", "Closed",
+          "SlightlyClosed", "Open", "Success", "ExcessiveCollisions")
+    from oracle.oracle import MODE_IDS
+    cases = js("classify")
+    base = {0: 0, 1: 9, 2: 21, 3: 30}
+    nsucc = {0: 4, 1: 5, 2: 3, 3: 3}
+    nmodes = {0: 9, 1: 12, 2: 9, 3: 9}
+    for drop in (False, True):
+        sel = [c for c in cases if (c["rules"] == "drop_catch_all") == drop]
+        rules = None
+        if drop:
+            rules = [[list(range(base[s], base[s] + nsucc[s])),
+                      list(range(base[s] + nsucc[s], base[s] + nmodes[s] - 1))] for s in range(4)]
+        lab = C.classify_lists([[EV.index(k) for k in c["kinds"]] for c in sel],
+                               [SUBTASKS.index(c["subtask"]) for c in sel],
+                               [c["d0"] if c["d0"] is not None else 0.0 for c in sel],
+                               [c["d0"] is None for c in sel], rules)
+        from paper_2412_13211_b200 import _lib as L
+        for i, c in enumerate(sel):
+            if "error" in c:
+                assert lab["status"][i] != 0, c
+                assert L.lib().tl_status_name(int(lab["status"][i])).decode() == c["error"][0]
+            else:
+                assert lab["status"][i] == 0, c
+                assert [MODE_IDS[lab["mode"][i]], bool(lab["flags"][i] & 1),
+                        bool(lab["flags"][i] & 2)] == c["result"], c
+
+
+def test_filter_cases(C):
+    from test_oracle_golden import filter_ints
+    dev = torch.device("cuda")
+    for case in js("filter"):
+        labels, spec = case["labels"], case["spec"]
+        order, rows, pool, pool_keys, rule_w, n_rules = filter_ints(labels, spec)
+        # dense buckets: pool p owns n_rules[subtask(p)] buckets
+        psub = {}
+        for j, r in enumerate(rows):
+            if r[3] >= 0:
+                psub[pool[j]] = r[2]
+        b0 = [0]
+        w = []
+        for p in range(len(pool_keys)):
+            s = psub[p]
+            b0.append(b0[-1] + int(n_rules[s]))
+            w.extend(rule_w[s * 16: s * 16 + int(n_rules[s])])
+        bucket = np.array([b0[pool[j]] + r[3] if r[3] >= 0 else -1 for j, r in enumerate(rows)], np.int32)
+        sel, ps = C.filter_select(torch.from_numpy(bucket).to(dev), int(b0[-1]),
+                                  torch.from_numpy(np.array(b0, np.int32)).to(dev),
+                                  torch.from_numpy(np.array(w if w else [1.0], np.float64)).to(dev),
+                                  spec["quota_per_target"])
+        sel = sel.cpu().numpy()
+        got = sorted(labels[rows[j][0]][0] for j in range(len(rows)) if sel[j])
+        assert got == case["selected"]
+        ps = ps.cpu().numpy()
+        short = [{"quota_key": k[0], "subtask": k[1], "requested": spec["quota_per_target"],
+                  "selected": int(ps[j]), "shortfall": spec["quota_per_target"] - int(ps[j])}
+                 for j, k in enumerate(pool_keys) if ps[j] < spec["quota_per_target"]]
+        assert short == case["shortfalls"]
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_fuzz_10k_vs_oracle(C, TH, kind):
+    """acceptance criterion 2 scale: 10k fuzz seeds per subtask, records
+    bit-exact and modes equal against the CPU oracle (tests/test_acceptance.py:46-67)."""
+    from oracle import oracle as O
+    from golden_data import from_oracle_records
+    from paper_2412_13211_b200.synth import FuzzConfig
+    n = 10000
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    sb = C.fuzz_batch(np.arange(n), kind, FuzzConfig(), TH(), cs)
+    total, modes, nev, nrec = O.fuzz_label_batch(0, n, kind, n_threads=8)
+    lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    assert np.all(lab["status"] == 0)
+    assert np.array_equal(lab["mode"], modes)
+    assert np.array_equal(lab["n_events"], nev)
+    assert np.array_equal(sb.records.n_rec.cpu().numpy(), nrec)
+    planes = sb.records.planes.cpu().numpy()
+    rs = sb.records.rec_start.cpu().numpy()
+    for seed in range(0, n, 97):
+        _, recs = O.fuzz(seed, kind)
+        p, _ = from_oracle_records(O, recs)
+        assert same_bits_f32(planes[:, rs[seed]:rs[seed] + len(recs)], p), seed
+
+
+def test_mode_histogram(C, TH):
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    sb = C.fuzz_batch(np.arange(3000), 1, FuzzConfig(), TH(), cs)
+    h = C.mode_histogram(sb.labels, 3000).cpu().numpy()
+    lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    assert np.array_equal(h, np.bincount(lab["mode"], minlength=39))
