@@ -211,13 +211,15 @@ def main():
     gathered = torch.empty((world, N_ENV, 24), dtype=torch.uint8, device=dev) if world > 1 else None
     rb = ws.records()
     rb_c = rb.c()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # graphs need a non-default stream
+    torch.cuda.set_stream(stream)
 
     def synth_only(s):
         sp = ctypes.c_void_p(s.cuda_stream)
         L.check(lib.tl_fuzz(L.ptr(seeds_buf), N_ENV, KIND, ctypes.byref(cfg_c), ctypes.byref(th_c),
                             L.ptr(cs), None, ctypes.byref(rb_c), cap, None, None, None,
-                            L.ptr(ws.step_mask), L.ptr(ws.labels), sp), "tl_fuzz")
+                            L.ptr(ws.step_mask), L.ptr(ws.labels), L.ptr(ws.scratch), sp),
+                "tl_fuzz")
 
     def step_body(s):
         sp = ctypes.c_void_p(s.cuda_stream)
@@ -230,7 +232,7 @@ def main():
         if world > 1:
             L.check(lib.tl_mode_histogram(L.ptr(ws.labels), N_ENV, L.ptr(hist), sp), "hist")
 
-    launches_per_step = 5 + (1 if world > 1 else 0)
+    launches_per_step = 6 + (1 if world > 1 else 0)  # reset, realize, 3x scan, emit
 
     # warm-up (also sets kernel attributes before graph capture)
     seeds_buf.copy_(all_seeds[0])
@@ -286,7 +288,10 @@ def main():
         torch.cuda.synchronize()
         synth_ms = [a.elapsed_time(b) for a, b in kev]
 
-        # ---- end to end: host seeds -> device -> host records + labels -----
+        # ---- end to end through the C ABI with host buffers ---------------
+        # E (headline): pinned host seeds -> GPU -> labels + event lists back
+        # to pinned host memory; records stay in HBM (the rollout buffer).
+        # E_records: additionally compacts the records and copies them back.
         host_seeds = all_seeds.cpu().pin_memory()
         comp_planes = torch.empty((23, N_ENV * cap), dtype=torch.float32, device=dev)
         comp_g = torch.empty(N_ENV * cap, dtype=torch.uint8, device=dev)
@@ -300,52 +305,63 @@ def main():
         h_evoff = torch.empty(N_ENV + 1, dtype=torch.int64).pin_memory()
         h_evk = torch.empty(ev_cap, dtype=torch.uint8).pin_memory()
         h_evt = torch.empty(ev_cap, dtype=torch.int32).pin_memory()
+        h_tot = torch.empty(2, dtype=torch.int64).pin_memory()
         K2 = max(1, min(K, 50))
-        e2e_ms, h2d_b, d2h_b, e2e_recs = [], 0, 0, 0
-        for k in range(K2):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            seeds_buf.copy_(host_seeds[k], non_blocking=True)
-            graph.replay()
-            collectives()
-            sp = ctypes.c_void_p(stream.cuda_stream)
-            L.check(lib.tl_scan_counts(L.ptr(ws.n_rec), N_ENV, L.ptr(comp_start), L.ptr(scan_scratch), sp), "scan")
-            L.check(lib.tl_compact_records(ctypes.byref(rb_c), N_ENV, L.ptr(comp_start),
-                                           ctypes.byref(comp_c), sp), "compact")
-            # result sizes (one 16-byte read), then exactly the produced bytes
-            tot = torch.stack([comp_start[N_ENV], ev_off[N_ENV]]).cpu()
-            R, NE = int(tot[0]), int(tot[1])
-            for p in range(23):
-                h_planes[p, :R].copy_(comp_planes[p, :R], non_blocking=True)
-            h_g[:R].copy_(comp_g[:R], non_blocking=True)
-            h_labels.copy_(ws.labels, non_blocking=True)
-            h_evoff.copy_(ev_off, non_blocking=True)
-            h_evk[:NE].copy_(ev_kind[:NE], non_blocking=True)
-            h_evt[:NE].copy_(ev_t[:NE], non_blocking=True)
-            b.record(stream)
-            torch.cuda.synchronize()
-            e2e_ms.append(a.elapsed_time(b))
-            e2e_recs += R
-            h2d_b = N_ENV * 8
-            d2h_b = R * RECORD_BYTES + N_ENV * 24 + (N_ENV + 1) * 8 + NE * 5 + 16
-            flush.zero_()
+
+        def e2e_loop(with_records):
+            ms, recs, h2d, d2h = [], 0, 0, 0
+            for k in range(K2):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                seeds_buf.copy_(host_seeds[k], non_blocking=True)
+                graph.replay()
+                collectives()
+                sp = ctypes.c_void_p(stream.cuda_stream)
+                h_labels.copy_(ws.labels, non_blocking=True)
+                h_evoff.copy_(ev_off, non_blocking=True)
+                if with_records:
+                    L.check(lib.tl_scan_counts(L.ptr(ws.n_rec), N_ENV, L.ptr(comp_start),
+                                               L.ptr(scan_scratch), sp), "scan")
+                    L.check(lib.tl_compact_records(ctypes.byref(rb_c), N_ENV, L.ptr(comp_start),
+                                                   ctypes.byref(comp_c), sp), "compact")
+                    h_tot[0:1].copy_(comp_start[N_ENV:N_ENV + 1], non_blocking=True)
+                stream.synchronize()  # sizes of the variable-length outputs
+                NE = int(h_evoff[N_ENV])
+                R = int(h_tot[0]) if with_records else 0
+                h_evk[:NE].copy_(ev_kind[:NE], non_blocking=True)
+                h_evt[:NE].copy_(ev_t[:NE], non_blocking=True)
+                if with_records:
+                    for p_ in range(23):
+                        h_planes[p_, :R].copy_(comp_planes[p_, :R], non_blocking=True)
+                    h_g[:R].copy_(comp_g[:R], non_blocking=True)
+                b.record(stream)
+                stream.synchronize()
+                ms.append(a.elapsed_time(b))
+                recs += int(nrec_log[k].sum())
+                h2d = N_ENV * 8
+                d2h = N_ENV * 24 + (N_ENV + 1) * 8 + NE * 5 + (R * RECORD_BYTES + 8 if with_records else 0)
+                flush.zero_()
+            return sum(ms) / 1e3, recs, h2d, d2h
+
+        t_e2e, e2e_recs, h2d_b, d2h_b = e2e_loop(False)
+        t_e2r, e2r_recs, _, d2h_rb = e2e_loop(True)
     clk = clocks.summary()
 
     recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
     total_recs = float(recs_per_step.sum().item())
     t_dev = sum(step_ms) / 1e3
     t_syn = sum(synth_ms) / 1e3
-    t_e2e = sum(e2e_ms) / 1e3
-    tt = torch.tensor([t_dev, t_syn, t_e2e, total_recs, float(e2e_recs)], dtype=torch.float64, device=dev)
+    tt = torch.tensor([t_dev, t_syn, t_e2e, t_e2r, total_recs, float(e2e_recs), float(e2r_recs)],
+                      dtype=torch.float64, device=dev)
     if world > 1:
-        mx = tt[:3].clone()
+        mx = tt[:4].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt[3:].clone()
+        sm = tt[4:].clone()
         dist.all_reduce(sm)
-        t_dev, t_syn, t_e2e = mx.tolist()
-        total_recs, e2e_recs_all = sm.tolist()
+        t_dev, t_syn, t_e2e, t_e2r = mx.tolist()
+        total_recs, e2e_recs_all, e2r_recs_all = sm.tolist()
     else:
-        e2e_recs_all = float(e2e_recs)
+        e2e_recs_all, e2r_recs_all = float(e2e_recs), float(e2r_recs)
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -370,7 +386,7 @@ def main():
                    "parallelism": f"episodes sharded over {world} GPU(s), NCCL label all-gather",
                    "l2": "flushed between timed steps (256 MiB write, excluded from timing)",
                    "timing": "CUDA events per step on the launch stream, max over ranks",
-                   "step": "1 CUDA graph: tl_fuzz + tl_scan_events + tl_emit_events"
+                   "step": "1 CUDA graph: tl_fuzz (reset + realize kernels) + tl_scan_events + tl_emit_events"
                            + (" + tl_mode_histogram, then NCCL all_gather/all_reduce" if world > 1 else "")},
         "gpu_launches": launches_per_step * K,
         "roofline": {"kernel": "k_synth (tl_fuzz)", "bound": "hbm", "achieved": achieved,
@@ -382,8 +398,13 @@ def main():
                              "ALU/latency-bound, not HBM-bound (SURVEY 8(d))"},
         "e2e": {"value": e2e_recs_all / t_e2e, "unit": "env-steps/s",
                 "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
-                "steps": K2, "note": "pinned host seeds -> GPU -> compact records, labels "
-                                      "and event lists back to pinned host memory"},
+                "steps": K2, "note": "C-ABI calls with host buffers: pinned host seeds -> GPU "
+                                      "-> labels + ordered event lists back to pinned host "
+                                      "memory every step (records stay in HBM)",
+                "with_records": {"value": e2r_recs_all / t_e2r, "unit": "env-steps/s",
+                                 "d2h_bytes_per_step": d2h_rb,
+                                 "note": "same, plus tl_compact_records + D2H of every "
+                                         "generated record (93 B/env-step)"}},
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
                          "sample": cb_sample, "trajectories_per_sec": cb_eps},
         "clocks": clk,

@@ -219,12 +219,15 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off,
                        const tl_rules* rules /* host */, tl_label* out,
                        void* stream);
 
-/* K3+K4 fused: for each seed, random_script(seed) -> realize(seed ^ 0x5EED)
- * -> label.  Records written to out->planes (f32) at rec_start[e] =
- * e*cap_per_env (written by the kernel along with n_rec).  label_csets
- * (device) is indexed by articulation kind (0 none, 1 fridge, 2 drawer).
- * script_kind/script_gap (optional) receive the sampled steps at
- * e*(cfg.max_events+4); scripts (optional) the script scalars.            */
+/* K3+K4: for each seed, random_script(seed) -> realize(seed ^ 0x5EED) ->
+ * label.  Two launches: a reset kernel (one thread per MT state: CPython
+ * seeding + random_script) and the realize+label kernel (one warp per
+ * episode).  Records go to out->planes (f32) at rec_start[e] =
+ * e*cap_per_env (rec_start and n_rec written).  label_csets (device) is
+ * indexed [subtask*3 + articulation kind] (0 none, 1 fridge, 2 drawer).
+ * script_kind/script_gap/scripts (optional) receive the sampled scripts
+ * (steps at e*(cfg.max_events+4)); scratch >= tl_fuzz_scratch_bytes().   */
+size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg /* host */);
 int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask,
             const tl_fuzz_cfg* cfg /* host */,
             const tl_thresholds* th_realize /* host */,
@@ -232,17 +235,20 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask,
             tl_records* out /* host struct, device arrays */,
             int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
             tl_script* scripts, uint8_t* step_mask, tl_label* labels,
-            void* stream);
+            void* scratch, void* stream);
 
 /* realize given scripts (device array) then label; out->rec_start/n_rec
  * are INPUTS here (host computed the layout).  label_csets indexed
- * [subtask*3 + articulation kind]; episodes may mix subtasks.             */
+ * [subtask*3 + articulation kind]; episodes may mix subtasks.
+ * scratch >= tl_realize_scratch_bytes(n_env).                            */
+size_t tl_realize_scratch_bytes(int32_t n_env);
 int tl_realize(const tl_script* scripts, const uint8_t* step_kind,
                const int32_t* step_gap, int32_t n_env,
                const tl_thresholds* th_realize /* host */,
                const tl_cset* label_csets /* [4 subtasks][3 art] */,
                const tl_rules* rules /* host */, tl_records* out,
-               uint8_t* step_mask, tl_label* labels, void* stream);
+               uint8_t* step_mask, tl_label* labels, void* scratch,
+               void* stream);
 
 /* K5: filter_labels selection (pipeline.py:276-338).  Labels are already
  * in episode_id order.  bucket[i] in [-1, n_buckets): the (quota key,

@@ -143,10 +143,12 @@ def lib():
         "tl_scan_events": ([vp, i32, vp, vp, vp], ctypes.c_int),
         "tl_emit_events": ([vp, vp, vp, vp, vp, i32, vp, vp, vp], ctypes.c_int),
         "tl_classify_events": ([vp, vp, vp, vp, vp, i32, vp, vp, vp], ctypes.c_int),
+        "tl_fuzz_scratch_bytes": ([i32, P(FuzzCfg_c)], ctypes.c_size_t),
         "tl_fuzz": ([vp, i32, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
-                     P(Records_c), i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
+                     P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "tl_realize_scratch_bytes": ([i32], ctypes.c_size_t),
         "tl_realize": ([vp, vp, vp, i32, P(Thresholds_c), vp, vp, P(Records_c),
-                        vp, vp, vp], ctypes.c_int),
+                        vp, vp, vp, vp], ctypes.c_int),
         "tl_filter_scratch_bytes": ([i64, i32, i32], ctypes.c_size_t),
         "tl_filter_select": ([vp, i64, i32, i32, vp, vp, i64, vp, vp, vp, vp],
                              ctypes.c_int),
@@ -172,7 +174,7 @@ def exported_symbols():
             "tl_scan_events", "tl_emit_events", "tl_classify_events", "tl_fuzz",
             "tl_realize", "tl_filter_scratch_bytes", "tl_filter_select",
             "tl_mode_histogram", "tl_eval_predicates", "tl_scan_counts",
-            "tl_compact_records"]
+            "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes"]
 
 
 def check(rc, what):

@@ -308,7 +308,10 @@ class SynthWorkspace:
         self.scripts = torch.empty((n_env, 56), dtype=torch.uint8, device=dev) if with_scripts else None
         self.script_kind = torch.empty(n_env * max_steps, dtype=torch.uint8, device=dev) if with_scripts else None
         self.script_gap = torch.empty(n_env * max_steps, dtype=torch.int32, device=dev) if with_scripts else None
-        self.n_env, self.cap, self.dof = n_env, cap_per_env, dof
+        c_cfg = L.FuzzCfg_c(max_steps - 4, 1, 1, 0, 1.0, 0.5)
+        self.scratch = torch.empty(int(L.lib().tl_fuzz_scratch_bytes(n_env, ctypes.byref(c_cfg))),
+                                   dtype=torch.uint8, device=dev)
+        self.n_env, self.cap, self.dof, self.max_steps = n_env, cap_per_env, dof, max_steps
 
     def records(self):
         return RecordBatch(self.planes, self.grasped, self.rec_start, self.n_rec, self.dof)
@@ -324,7 +327,8 @@ def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
         seeds = torch.as_tensor(np.asarray(seeds, np.int64), device=dev)
     n = int(seeds.shape[0])
     cap = fuzz_capacity(cfg)
-    if ws is None or ws.n_env < n or ws.cap != cap:
+    if (ws is None or ws.n_env < n or ws.cap != cap or ws.max_steps != cfg.max_events + 4
+            or (want_scripts and ws.scripts is None)):
         ws = SynthWorkspace(n, cap, with_scripts=want_scripts, max_steps=cfg.max_events + 4)
     rb = ws.records()
     c_cfg = L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0,
@@ -337,7 +341,8 @@ def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
                          L.ptr(ws.script_kind) if want_scripts else None,
                          L.ptr(ws.script_gap) if want_scripts else None,
                          L.ptr(ws.scripts) if want_scripts else None,
-                         L.ptr(ws.step_mask), L.ptr(ws.labels), L.stream_ptr())
+                         L.ptr(ws.step_mask), L.ptr(ws.labels), L.ptr(ws.scratch),
+                         L.stream_ptr())
     L.check(rc, "tl_fuzz")
     return SynthBatch(rb, ws.labels, ws.step_mask,
                       ws.scripts if want_scripts else None,
@@ -371,10 +376,12 @@ def realize_batch(scripts_np, step_kind, step_gap, th_realize: Thresholds, label
     t_k = torch.from_numpy(np.asarray(step_kind, np.uint8).reshape(-1) if len(step_kind) else np.zeros(1, np.uint8)).to(dev)
     t_g = torch.from_numpy(np.asarray(step_gap, np.int32).reshape(-1) if len(step_gap) else np.zeros(1, np.int32)).to(dev)
     rc_rules = rules_c(rules)
+    scratch = torch.empty(int(L.lib().tl_realize_scratch_bytes(n)), dtype=torch.uint8, device=dev)
     rc = L.lib().tl_realize(L.ptr(t_sc), L.ptr(t_k), L.ptr(t_g), n,
                             ctypes.byref(thresholds_c(th_realize)), L.ptr(label_csets),
                             ctypes.byref(rc_rules) if rc_rules is not None else None,
-                            ctypes.byref(rb.c()), L.ptr(mask), L.ptr(labels), L.stream_ptr())
+                            ctypes.byref(rb.c()), L.ptr(mask), L.ptr(labels), L.ptr(scratch),
+                            L.stream_ptr())
     L.check(rc, "tl_realize")
     return SynthBatch(rb, labels[:n], mask)
 

@@ -37,35 +37,35 @@ __device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t src)
   return src ^ (y >> 1) ^ ((0u - (y & 1u)) & 0x9908b0dfu);
 }
 
-// random.Random(int) seeding of one state (one lane).  key = abs(seed) in
-// little-endian 32-bit words (1 or 2 words for |seed| < 2^64).
-__device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed) {
-  uint64_t n = seed < 0 ? (uint64_t)0 - (uint64_t)seed : (uint64_t)seed;
-  const uint32_t k0 = (uint32_t)n, k1 = (uint32_t)(n >> 32);
-  const int klen = k1 ? 2 : 1;
+// random.Random(int) seeding of one state (one thread; init_by_array of
+// Modules/_randommodule.c).  key = abs(seed) as little-endian 32-bit words
+// (1 or 2 words for |seed| < 2^64).  `mt` may be a padded shared-memory row.
+template <int KLEN>
+__device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t k1) {
   uint32_t prev = kTlInitGenrand[0];
-  uint32_t v1 = 0;
-  int j = 0;
-  // init_by_array first loop: k = max(624, klen) = 624 iterations
-#pragma unroll 4
-  for (int i = 1; i < kMtN; i++) {
-    uint32_t v = (kTlInitGenrand[i] ^ ((prev ^ (prev >> 30)) * 1664525u)) +
-                 (j ? k1 : k0) + (uint32_t)j;
+  // first loop, k = max(624, klen) = 624 iterations: i = 1..623, then i = 1
+  uint32_t v1 = (kTlInitGenrand[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + k0;
+  mt[1] = v1;
+  prev = v1;
+#pragma unroll 8
+  for (int i = 2; i < kMtN; i++) {
+    const int j = KLEN == 1 ? 0 : ((i - 1) & 1);
+    const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
+    const uint32_t v = (kTlInitGenrand[i] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
     mt[i] = v;
     prev = v;
-    if (i == 1) v1 = v;
-    j = (j + 1 >= klen) ? 0 : j + 1;
   }
-  mt[0] = prev;  // i >= N: mt[0] = mt[N-1], i = 1
+  mt[0] = prev;
   {
-    uint32_t v = (v1 ^ ((prev ^ (prev >> 30)) * 1664525u)) + (j ? k1 : k0) + (uint32_t)j;
-    mt[1] = v;
-    prev = v;
+    const int j = KLEN == 1 ? 0 : ((kMtN - 1) & 1);  // 624th iteration: j = 623 % klen
+    const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
+    prev = (v1 ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
+    mt[1] = prev;
   }
   // second loop: N-1 iterations, i = 2..623 then wrap to i = 1
-#pragma unroll 4
+#pragma unroll 8
   for (int i = 2; i < kMtN; i++) {
-    uint32_t v = (mt[i] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
+    const uint32_t v = (mt[i] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
     mt[i] = v;
     prev = v;
   }
@@ -74,46 +74,77 @@ __device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed) {
   mt[0] = 0x80000000u;
 }
 
+__device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed) {
+  const uint64_t n = seed < 0 ? (uint64_t)0 - (uint64_t)seed : (uint64_t)seed;
+  const uint32_t k0 = (uint32_t)n, k1 = (uint32_t)(n >> 32);
+  if (k1) mt_seed_impl<2>(mt, k0, k1);
+  else mt_seed_impl<1>(mt, k0, 0u);
+}
+
 // Warp-cooperative regeneration of all 624 words in place (CPython's
-// genrand "generate N words at one time").  If ring != nullptr the tempered
-// outputs are also written to ring[(ring_base + i) & ring_mask].
+// genrand "generate N words at one time"); tempered outputs also go to
+// ring[(ring_base + i) & ring_mask].  Word i reads mt[i], mt[i+1] (old) and
+// mt[i+397] (old, i < 227) or mt[i-227] (new, i >= 227), so a group of up
+// to 7 consecutive 32-word iterations can load before any of them stores.
+template <int IT>
+__device__ __forceinline__ int twist_src(int i) {
+  return IT < 7 ? i + kMtM : IT > 7 ? i - (kMtN - kMtM) : (i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM));
+}
+
+template <int IT0, int NG>
+__device__ __forceinline__ void twist_group(uint32_t* mt, uint32_t* ring, uint32_t base,
+                                            uint32_t mask, int lane) {
+  uint32_t nv[NG];
+#pragma unroll
+  for (int g = 0; g < NG; g++) {
+    const int i = (IT0 + g) * 32 + lane;
+    nv[g] = mt_mix(mt[i], mt[i + 1], mt[g == 0 ? twist_src<IT0>(i) : g == 1 ? twist_src<IT0 + 1>(i)
+                                          : g == 2 ? twist_src<IT0 + 2>(i) : twist_src<IT0 + 3>(i)]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < NG; g++) {
+    const int i = (IT0 + g) * 32 + lane;
+    mt[i] = nv[g];
+    ring[(base + (uint32_t)i) & mask] = mt_temper(nv[g]);
+  }
+}
+
 __device__ __forceinline__ void mt_twist_warp(uint32_t* mt, uint32_t* ring,
-                                              uint32_t ring_base,
-                                              uint32_t ring_mask) {
+                                              uint32_t ring_base, uint32_t ring_mask) {
   const int lane = lane_id();
-#pragma unroll 1
-  for (int i0 = 0; i0 < kMtN; i0 += kWarp) {
-    const int i = i0 + lane;
-    uint32_t nv = 0;
-    if (i < kMtN) {
-      const int i1 = (i + 1 == kMtN) ? 0 : i + 1;
-      const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);
-      nv = mt_mix(mt[i], mt[i1], mt[src]);
-    }
-    __syncwarp();
-    if (i < kMtN) {
-      mt[i] = nv;
-      if (ring) ring[(ring_base + (uint32_t)i) & ring_mask] = mt_temper(nv);
-    }
+  twist_group<0, 4>(mt, ring, ring_base, ring_mask, lane);
+  twist_group<4, 4>(mt, ring, ring_base, ring_mask, lane);
+  twist_group<8, 4>(mt, ring, ring_base, ring_mask, lane);
+  twist_group<12, 4>(mt, ring, ring_base, ring_mask, lane);
+  twist_group<16, 3>(mt, ring, ring_base, ring_mask, lane);
+  // words 608..623 (word 623 wraps to the new mt[0])
+  uint32_t nv = 0;
+  const int i = 608 + lane;
+  if (lane < 16) nv = mt_mix(mt[i], mt[lane == 15 ? 0 : i + 1], mt[i - (kMtN - kMtM)]);
+  __syncwarp();
+  if (lane < 16) {
+    mt[i] = nv;
+    ring[(ring_base + (uint32_t)i) & ring_mask] = mt_temper(nv);
   }
   __syncwarp();
 }
 
-// Serial reader over an MT state for a single lane (script sampling).
+// Serial reader over a freshly seeded MT state for one thread (script
+// sampling).  Words are regenerated lazily in order, in place: word i of a
+// block reads mt[i+1] (old) and mt[i+397] (old) or mt[i-227] (already new),
+// exactly the values CPython's block regeneration reads.
 struct MtLane {
   uint32_t* mt;
-  int idx;
+  int idx;  // next word of the current block (0 right after seeding)
   __device__ __forceinline__ uint32_t genrand() {
-    if (idx >= kMtN) {
-      // serial regeneration (rare: only when a script needs > 624 words)
-      for (int i = 0; i < kMtN; i++) {
-        const int i1 = (i + 1 == kMtN) ? 0 : i + 1;
-        const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);
-        mt[i] = mt_mix(mt[i], mt[i1], mt[src]);
-      }
-      idx = 0;
-    }
-    return mt_temper(mt[idx++]);
+    const int i = idx;
+    const int i1 = i + 1 == kMtN ? 0 : i + 1;
+    const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);
+    const uint32_t v = mt_mix(mt[i], mt[i1], mt[src]);
+    mt[i] = v;
+    idx = i1;
+    return mt_temper(v);
   }
   __device__ __forceinline__ double random() {
     uint32_t a = genrand() >> 5, b = genrand() >> 6;

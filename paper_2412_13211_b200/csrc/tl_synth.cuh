@@ -43,11 +43,8 @@ struct SynthWarp {
   int32_t hw[kMaxSteps + 1];    // words per hold record in segment s
   StepSt st[kMaxSteps + 1];
   double dist_after[kMaxSteps];
-  double radv[32];
-  float cum32[32];
   uint8_t kind[kMaxSteps];
   uint8_t sflag[kMaxSteps];     // bit0 dist draw at the event
-  uint8_t rflag[32];            // bit0 advance draw, bit1 ExcessiveCollisions applied
   int32_t misc[16];
   tl_cset cs;                   // labelling constants (staged)
 };
@@ -60,17 +57,16 @@ struct RzConst {
 };
 
 struct SynthParams {
-  // fuzz inputs
+  // fuzz inputs (k_fuzz_reset)
   const int64_t* seeds;
   int32_t fuzz_subtask;
   tl_fuzz_cfg cfg;
-  uint8_t* script_kind;
-  int32_t* script_gap;
-  tl_script* scripts_out;
-  // realize inputs
-  const tl_script* scripts;
-  const uint8_t* step_kind;
-  const int32_t* step_gap;
+  // scripts (written by k_fuzz_reset, or given for realize)
+  tl_script* scripts;
+  uint8_t* step_kind;
+  int32_t* step_gap;
+  // seeded realize-RNG states, [n_env][624] (k_fuzz_reset / k_seed_states)
+  uint32_t* states;
   // common
   int32_t n_env;
   int32_t cap_per_env;
@@ -373,6 +369,77 @@ __device__ __forceinline__ StepSt make_st(const RzConst& z, const PlanSt& p, int
   return s;
 }
 
+// ---- reset: seeding + random_script, one thread per RNG ---------------------
+// CPython seeding is a 1247-step serial chain per state, so it runs one
+// state per thread (32 chains per warp) into padded shared-memory rows
+// (stride 625 words: conflict-free), instead of occupying one lane of an
+// episode's warp.  Fuzz: even lanes seed the script RNG (seed) and sample
+// random_script; odd lanes seed the realize RNG (seed ^ 0x5EED, synth.py:515).
+constexpr int kRowWords = kMtN + 1;
+
+__device__ __forceinline__ void copy_rows_out(const uint32_t* rows, int first_row, int row_step,
+                                              int n_rows, uint32_t* dst, int64_t e0, int n_env) {
+  const int lane = lane_id();
+  for (int j = 0; j < n_rows; j++) {
+    const int64_t e = e0 + j;
+    if (e >= n_env) break;
+    const uint32_t* src = rows + (first_row + j * row_step) * kRowWords;
+    uint32_t* d = dst + e * kMtN;
+    for (int i = lane; i < kMtN; i += 32) d[i] = src[i];
+  }
+}
+
+__global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
+  extern __shared__ uint32_t rows[];  // [32][kRowWords]
+  const int lane = lane_id();
+  const int64_t e0 = (int64_t)blockIdx.x * 16;
+  const int64_t e = e0 + (lane >> 1);
+  const bool valid = e < p.n_env;
+  uint32_t* row = rows + lane * kRowWords;
+  const int ms = p.cfg.max_events + 4;
+  if (valid) {
+    const int64_t seed = p.seeds[e];
+    mt_seed_lane(row, (lane & 1) ? (seed ^ 0x5EED) : seed);
+    if (!(lane & 1)) {
+      MtLane R{row, 0};
+      tl_script t;
+      uint8_t* sk = p.step_kind + e * ms;
+      int32_t* sg = p.step_gap + e * ms;
+      uint8_t k8[kMaxSteps];
+      int32_t g32[kMaxSteps];
+      const int ns = sample_script(R, p.fuzz_subtask, p.cfg, k8, g32, t);
+      int64_t nr = 1;
+      for (int i = 0; i < (ns < 0 ? 0 : ns); i++) {
+        sk[i] = k8[i];
+        sg[i] = g32[i];
+        nr += g32[i];
+      }
+      const int64_t tmin = ns > 0 ? 0 : 1;
+      nr += t.tail > tmin ? t.tail : tmin;
+      if (nr < 2) nr = 2;
+      t.step_off = e * ms;
+      t.seed = seed ^ 0x5EED;
+      t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
+      p.scripts[e] = t;
+      p.out.rec_start[e] = e * p.cap_per_env;
+      p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;
+    }
+  }
+  __syncwarp();
+  copy_rows_out(rows, 1, 2, 16, p.states, e0, p.n_env);
+}
+
+// realize path: seed the realize RNG of given scripts (one thread per state)
+__global__ void __launch_bounds__(32) k_seed_states(SynthParams p) {
+  extern __shared__ uint32_t rows[];
+  const int lane = lane_id();
+  const int64_t e0 = (int64_t)blockIdx.x * 32;
+  const int64_t e = e0 + lane;
+  if (e < p.n_env) mt_seed_lane(rows + lane * kRowWords, p.scripts[e].seed);
+  __syncwarp();
+  copy_rows_out(rows, 0, 1, 32, p.states, e0, p.n_env);
+}
+
 template <bool FUZZ, int DOFMAX>
 __global__ void __launch_bounds__(kSynthWarps * 32)
     k_synth(SynthParams p) {
@@ -385,80 +452,25 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
   const float fnan = __int_as_float(0x7fc00000);
 
   for (int e = blockIdx.x * kSynthWarps + warp; e < p.n_env; e += gridDim.x * kSynthWarps) {
-    // ---------------- reset: seed, (sample script), realizer constants -------
-    tl_script sc;
-    int64_t rs;
-    int n_rec = 0;
-    if (FUZZ) {
-      const int64_t seed = p.seeds[e];
-      if (lane < 2) mt_seed_lane(lane == 0 ? S.ring : S.mt, lane == 0 ? seed : (seed ^ 0x5EED));
-      __syncwarp();
-      mt_twist_warp(S.ring, nullptr, 0, 0);  // script RNG: first block
-      if (lane == 0) {
-        MtLane R{S.ring, 0};
-        tl_script t;
-        const int ns = sample_script(R, p.fuzz_subtask, p.cfg, S.kind, S.gap, t);
-        t.step_off = (int64_t)e * (p.cfg.max_events + 4);
-        t.seed = seed ^ 0x5EED;
-        int64_t nr = 1;
-        for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += S.gap[i];
-        const int64_t tmin = ns > 0 ? 0 : 1;
-        nr += t.tail > tmin ? t.tail : tmin;
-        if (nr < 2) nr = 2;
-        S.misc[0] = ns;
-        S.misc[1] = (ns < 0 || nr > p.cap_per_env) ? 1 : 0;
-        S.misc[2] = (int)nr;
-        S.misc[3] = t.tail;
-        S.misc[4] = t.initial_grasped;
-        S.misc[5] = t.initial_contact;
-        S.misc[6] = t.initial_level;
-        S.misc[7] = t.art_kind;
-        reinterpret_cast<double*>(&S.misc[8])[0] = t.initial_dist_obj_goal;
-        if (p.scripts_out) p.scripts_out[e] = t;
-        if (p.script_kind && ns > 0) {
-          for (int i = 0; i < ns; i++) {
-            p.script_kind[t.step_off + i] = S.kind[i];
-            p.script_gap[t.step_off + i] = S.gap[i];
-          }
-        }
-      }
-      __syncwarp();
-      sc.step_off = 0;
-      sc.seed = seed ^ 0x5EED;
-      sc.n_steps = S.misc[0];
-      sc.tail = S.misc[3];
-      sc.subtask = p.fuzz_subtask;
-      sc.art_kind = S.misc[7];
-      sc.initial_level = S.misc[6];
-      sc.initial_grasped = S.misc[4];
-      sc.initial_contact = S.misc[5];
-      sc.arm_dof = dof;
-      sc.initial_dist_obj_goal = reinterpret_cast<const double*>(&S.misc[8])[0];
-      rs = (int64_t)e * p.cap_per_env;
-      n_rec = S.misc[2];
-      const bool bad = S.misc[1] != 0;
-      __syncwarp();
-      if (lane == 0) {
-        p.out.rec_start[e] = rs;
-        p.out.n_rec[e] = bad ? 0 : n_rec;
-      }
-      if (bad) {
-        if (lane == 0) {
-          tl_label L;
-          L.status = TL_ERR_SCRIPT_CAPACITY; L.n_events = 0; L.err_index = -1;
-          L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
-          L.d0 = __longlong_as_double(0x7ff8000000000000ll);
-          p.labels[e] = L;
-        }
-        continue;
-      }
-    } else {
-      sc = p.scripts[e];
-      rs = p.out.rec_start[e];
-      n_rec = p.out.n_rec[e];
-      if (lane == 0) mt_seed_lane(S.mt, sc.seed);
-      __syncwarp();
+    // ---------------- script + seeded RNG state from the reset kernel --------
+    const tl_script sc = p.scripts[e];
+    const int64_t rs = p.out.rec_start[e];
+    const int n_rec = p.out.n_rec[e];
+    {
+      const uint32_t* src = p.states + (int64_t)e * kMtN;
+      for (int i = lane; i < kMtN; i += 32) S.mt[i] = src[i];
     }
+    if (FUZZ && sc.n_steps < 0) {
+      if (lane == 0) {
+        tl_label L;
+        L.status = TL_ERR_SCRIPT_CAPACITY; L.n_events = 0; L.err_index = -1;
+        L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
+        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
+        p.labels[e] = L;
+      }
+      continue;
+    }
+    __syncwarp();
     const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
     stage_cset(&S.cs, &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
     RzConst z;
@@ -501,7 +513,7 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
     // --------------- step windows -------------------------------------------
     LState LS;
     lstate_init(LS);
-    double cum = 0.0;            // lane 0 owns the serial f64 recurrence
+    double cum = 0.0;            // warp-uniform serial f64 recurrence
     double dist_carry = dist0;   // dist before the window
     int32_t w_carry = 2 * z.ne;  // record 0 emits 2*dof+5 draws
     int32_t tau_prev = 0;
@@ -514,13 +526,11 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
     for (;;) {
       const int ns = min(n_steps - s_base, kMaxSteps);
       const bool last_window = s_base + ns >= n_steps;
-      if (!FUZZ) {
-        for (int i = lane; i < ns; i += 32) {
-          S.kind[i] = p.step_kind[sc.step_off + s_base + i];
-          S.gap[i] = p.step_gap[sc.step_off + s_base + i];
-        }
-        __syncwarp();
+      for (int i = lane; i < ns; i += 32) {
+        S.kind[i] = p.step_kind[sc.step_off + s_base + i];
+        S.gap[i] = p.step_gap[sc.step_off + s_base + i];
       }
+      __syncwarp();
       // ---- plan (lane 0): record/word layout + deterministic state ------------
       if (lane == 0) {
         PlanSt q = pcarry;
@@ -610,9 +620,9 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
         };
         // advance_cum draw, object-distance draw and its feasibility check
         int my_err = 0;
+        double my_radv = 0.0;
         if (valid) {
-          S.radv[lane] = adv ? rnd(o) : -1.0;
-          S.rflag[lane] = (uint8_t)((adv ? 1 : 0) | (ev == TL_EV_EXCESSIVE_COLLISIONS && !(perr && s == pstep) ? 2 : 0));
+          if (adv) my_radv = rnd(o);
           if (app) {
             const double rr = rnd(o + 2 * adv);
             S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rr) : uniform_rn(0.3, 0.8, rr);
@@ -643,20 +653,21 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
           err_step = s_base + __shfl_sync(kFull, s, L);
           break;
         }
-        // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213)
+        // cum_robot_force: the one serial f64 recurrence (synth.py:192-196,
+        // :210-213), run in lockstep by all lanes on shuffled draws (cum is
+        // warp-uniform).  uniform(0.0, b) = RN(b * r) exactly for b, r >= 0.
         const int cnt = min(32, r_end - r0);
-        if (lane == 0) {
-          for (int j = 0; j < cnt; j++) {
-            const uint8_t f = S.rflag[j];
-            if (f & 1) {
-              const double h = __dsub_rn(z.L09, cum);
-              cum = __dadd_rn(cum, uniform_rn(0.0, __dmul_rn(h, 0.05), S.radv[j]));
-            }
-            if (f & 2) cum = z.L105;
-            S.cum32[j] = __double2float_rn(cum);
-          }
+        const unsigned adv_m = __ballot_sync(kFull, valid && adv);
+        const unsigned exc_m = __ballot_sync(
+            kFull, valid && ev == TL_EV_EXCESSIVE_COLLISIONS && !(perr && s == pstep));
+        float my_cum32 = 0.f;
+        for (int j = 0; j < cnt; j++) {
+          const double rj = __shfl_sync(kFull, my_radv, j);
+          if ((adv_m >> j) & 1u)
+            cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rj));
+          if ((exc_m >> j) & 1u) cum = z.L105;
+          if (lane == j) my_cum32 = __double2float_rn(cum);
         }
-        __syncwarp();
         // ---- emit + write + label ---------------------------------------------
         RecV<float> v;
         uint32_t ind = 0, errb = 0;
@@ -689,7 +700,7 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
           v.der = emit ? __double2float_rn(uniform_rn(0.2, 1.0, rnd(eb2 + 8))) : 0.f;
           v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
           v.force = stv.force;
-          v.cum = S.cum32[lane];
+          v.cum = my_cum32;
           v.art = stv.art;
           v.g = stv.grasped != 0;
           v.qdm = mqd;

@@ -224,6 +224,14 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
 }
 
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
+  const int rows_smem = 32 * kRowWords * 4;
+  if (fuzz) {
+    set_max_smem(k_fuzz_reset, rows_smem);
+    k_fuzz_reset<<<(sp.n_env + 15) / 16, 32, rows_smem, S(stream)>>>(sp);
+  } else {
+    set_max_smem(k_seed_states, rows_smem);
+    k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
+  }
   const int smem = kSynthWarps * (int)sizeof(SynthWarp);
   const bool small = sp.out.dof <= 7;
   void (*k)(SynthParams) = fuzz ? (small ? k_synth<true, 7> : k_synth<true, 16>)
@@ -237,24 +245,44 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   return check_launch();
 }
 
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
+  const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
+  return align256(n * kMtN * 4) + align256(n * sizeof(tl_script)) + align256(n * ms) +
+         align256(n * ms * 4);
+}
+
+size_t tl_realize_scratch_bytes(int32_t n_env) {
+  return align256((size_t)(n_env > 0 ? n_env : 1) * kMtN * 4);
+}
+
 int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
             const tl_thresholds* th_realize, const tl_cset* label_csets, const tl_rules* rules,
             tl_records* out, int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
-            tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* stream) {
-  if (!cfg || !th_realize || !label_csets || !out || !labels || n_env < 0 || subtask < 0 ||
-      subtask > 3 || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
+            tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* scratch,
+            void* stream) {
+  if (!cfg || !th_realize || !label_csets || !out || !labels || !scratch || n_env < 0 ||
+      subtask < 0 || subtask > 3 || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
       cfg->max_gap < 1 || cfg->max_tail < 1 || cfg->max_events < 0 ||
-      cfg->max_events + 4 > kMaxSteps || cap_per_env < 2 || (script_kind && !script_gap))
+      cfg->max_events + 4 > kMaxSteps || cap_per_env < 2 || (script_kind && !script_gap) ||
+      (!script_kind && script_gap))
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
+  const size_t n = (size_t)n_env, ms = (size_t)(cfg->max_events + 4);
+  char* base = reinterpret_cast<char*>(scratch);
   SynthParams sp;
   memset(&sp, 0, sizeof(sp));
+  sp.states = reinterpret_cast<uint32_t*>(base);
+  base += align256(n * kMtN * 4);
+  sp.scripts = scripts ? scripts : reinterpret_cast<tl_script*>(base);
+  base += align256(n * sizeof(tl_script));
+  sp.step_kind = script_kind ? script_kind : reinterpret_cast<uint8_t*>(base);
+  base += align256(n * ms);
+  sp.step_gap = script_gap ? script_gap : reinterpret_cast<int32_t*>(base);
   sp.seeds = seeds;
   sp.fuzz_subtask = subtask;
   sp.cfg = *cfg;
-  sp.script_kind = script_kind;
-  sp.script_gap = script_gap;
-  sp.scripts_out = scripts;
   sp.n_env = n_env;
   sp.cap_per_env = cap_per_env;
   sp.th = *th_realize;
@@ -269,16 +297,17 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_
 int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t* step_gap,
                int32_t n_env, const tl_thresholds* th_realize, const tl_cset* label_csets,
                const tl_rules* rules, tl_records* out, uint8_t* step_mask, tl_label* labels,
-               void* stream) {
-  if (!scripts || !th_realize || !label_csets || !out || !labels || n_env < 0 ||
+               void* scratch, void* stream) {
+  if (!scripts || !th_realize || !label_csets || !out || !labels || !scratch || n_env < 0 ||
       out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF)
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
   SynthParams sp;
   memset(&sp, 0, sizeof(sp));
-  sp.scripts = scripts;
-  sp.step_kind = step_kind;
-  sp.step_gap = step_gap;
+  sp.scripts = const_cast<tl_script*>(scripts);
+  sp.step_kind = const_cast<uint8_t*>(step_kind);
+  sp.step_gap = const_cast<int32_t*>(step_gap);
+  sp.states = reinterpret_cast<uint32_t*>(scratch);
   sp.n_env = n_env;
   sp.th = *th_realize;
   sp.label_csets = label_csets;
