@@ -224,15 +224,13 @@ def main():
     def step_body(s):
         sp = ctypes.c_void_p(s.cuda_stream)
         synth_only(s)
-        L.check(lib.tl_scan_events(L.ptr(ws.labels), N_ENV, L.ptr(ev_off), L.ptr(scan_scratch), sp),
-                "scan")
-        L.check(lib.tl_emit_events(L.ptr(ws.step_mask), L.ptr(ws.rec_start), L.ptr(ws.n_rec),
-                                   L.ptr(ws.labels), L.ptr(ev_off), N_ENV, L.ptr(ev_kind),
-                                   L.ptr(ev_t), sp), "emit")
+        L.check(lib.tl_scan_emit_events(L.ptr(ws.step_mask), L.ptr(ws.rec_start), L.ptr(ws.n_rec),
+                                        L.ptr(ws.labels), N_ENV, L.ptr(ev_off), L.ptr(ev_kind),
+                                        L.ptr(ev_t), L.ptr(scan_scratch), sp), "scan_emit")
         if world > 1:
             L.check(lib.tl_mode_histogram(L.ptr(ws.labels), N_ENV, L.ptr(hist), sp), "hist")
 
-    launches_per_step = 6 + (1 if world > 1 else 0)  # reset, realize, 3x scan, emit
+    launches_per_step = 3 + (1 if world > 1 else 0)  # reset, realize, scan+emit
 
     # warm-up (also sets kernel attributes before graph capture)
     seeds_buf.copy_(all_seeds[0])
@@ -386,7 +384,7 @@ def main():
                    "parallelism": f"episodes sharded over {world} GPU(s), NCCL label all-gather",
                    "l2": "flushed between timed steps (256 MiB write, excluded from timing)",
                    "timing": "CUDA events per step on the launch stream, max over ranks",
-                   "step": "1 CUDA graph: tl_fuzz (reset + realize kernels) + tl_scan_events + tl_emit_events"
+                   "step": "1 CUDA graph: tl_fuzz (reset + realize kernels) + tl_scan_emit_events"
                            + (" + tl_mode_histogram, then NCCL all_gather/all_reduce" if world > 1 else "")},
         "gpu_launches": launches_per_step * K,
         "roofline": {"kernel": "k_synth (tl_fuzz)", "bound": "hbm", "achieved": achieved,

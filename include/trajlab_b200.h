@@ -212,6 +212,13 @@ int tl_emit_events(const uint8_t* step_mask, const int64_t* rec_start,
                    const int64_t* ev_off, int32_t n_env, uint8_t* ev_kind,
                    int32_t* ev_t, void* stream);
 
+/* tl_scan_events + tl_emit_events in one launch (single-pass decoupled
+ * look-back scan, then emission); scratch >= tl_scan_scratch_bytes(n).    */
+int tl_scan_emit_events(const uint8_t* step_mask, const int64_t* rec_start,
+                        const int32_t* n_rec, const tl_label* labels,
+                        int32_t n_env, int64_t* ev_off, uint8_t* ev_kind,
+                        int32_t* ev_t, void* scratch, void* stream);
+
 /* classify given event lists: kinds at [ev_off[e], ev_off[e+1]). */
 int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off,
                        const uint8_t* subtask, const double* d0,

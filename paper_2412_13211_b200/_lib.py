@@ -142,6 +142,7 @@ def lib():
         "tl_scan_scratch_bytes": ([i32], ctypes.c_size_t),
         "tl_scan_events": ([vp, i32, vp, vp, vp], ctypes.c_int),
         "tl_emit_events": ([vp, vp, vp, vp, vp, i32, vp, vp, vp], ctypes.c_int),
+        "tl_scan_emit_events": ([vp, vp, vp, vp, i32, vp, vp, vp, vp, vp], ctypes.c_int),
         "tl_classify_events": ([vp, vp, vp, vp, vp, i32, vp, vp, vp], ctypes.c_int),
         "tl_fuzz_scratch_bytes": ([i32, P(FuzzCfg_c)], ctypes.c_size_t),
         "tl_fuzz": ([vp, i32, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
@@ -174,7 +175,8 @@ def exported_symbols():
             "tl_scan_events", "tl_emit_events", "tl_classify_events", "tl_fuzz",
             "tl_realize", "tl_filter_scratch_bytes", "tl_filter_select",
             "tl_mode_histogram", "tl_eval_predicates", "tl_scan_counts",
-            "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes"]
+            "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes",
+            "tl_scan_emit_events"]
 
 
 def check(rc, what):

@@ -222,15 +222,27 @@ def emit_events(rb: RecordBatch, res: LabelResult, ev_capacity=None):
     dev = rb.planes.device
     n = rb.n_env
     ev_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
-    scratch = torch.empty(max(1, L.lib().tl_scan_scratch_bytes(n)), dtype=torch.uint8, device=dev)
-    L.check(L.lib().tl_scan_events(L.ptr(res.labels), n, L.ptr(ev_off), L.ptr(scratch),
-                                   L.stream_ptr()), "tl_scan_events")
-    total = int(ev_off[n].item()) if ev_capacity is None else int(ev_capacity)
-    ev_kind = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
-    ev_t = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
-    L.check(L.lib().tl_emit_events(L.ptr(res.step_mask), L.ptr(rb.rec_start), L.ptr(rb.n_rec),
-                                   L.ptr(res.labels), L.ptr(ev_off), n, L.ptr(ev_kind),
-                                   L.ptr(ev_t), L.stream_ptr()), "tl_emit_events")
+    scratch = torch.empty(max(16, L.lib().tl_scan_scratch_bytes(n)), dtype=torch.uint8, device=dev)
+    if ev_capacity is None:
+        # exact-size outputs: scan, read the total, then emit
+        L.check(L.lib().tl_scan_events(L.ptr(res.labels), n, L.ptr(ev_off), L.ptr(scratch),
+                                       L.stream_ptr()), "tl_scan_events")
+        total = int(ev_off[n].item())
+        ev_kind = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+        ev_t = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        L.check(L.lib().tl_emit_events(L.ptr(res.step_mask), L.ptr(rb.rec_start),
+                                       L.ptr(rb.n_rec), L.ptr(res.labels), L.ptr(ev_off), n,
+                                       L.ptr(ev_kind), L.ptr(ev_t), L.stream_ptr()),
+                "tl_emit_events")
+    else:
+        # capacity-bounded outputs: one fused launch, no host round trip
+        ev_kind = torch.empty(max(int(ev_capacity), 1), dtype=torch.uint8, device=dev)
+        ev_t = torch.empty(max(int(ev_capacity), 1), dtype=torch.int32, device=dev)
+        L.check(L.lib().tl_scan_emit_events(L.ptr(res.step_mask), L.ptr(rb.rec_start),
+                                            L.ptr(rb.n_rec), L.ptr(res.labels), n,
+                                            L.ptr(ev_off), L.ptr(ev_kind), L.ptr(ev_t),
+                                            L.ptr(scratch), L.stream_ptr()),
+                "tl_scan_emit_events")
     res.ev_off, res.ev_kind, res.ev_t = ev_off, ev_kind, ev_t
     return res
 

@@ -755,3 +755,88 @@ __global__ void __launch_bounds__(256)
 }
 
 }  // namespace tl
+
+namespace tl {
+
+// ---- K2 fused: event-offset scan (decoupled look-back) + event emission -------
+// One block = 32 warps = a tile of 32 episodes.  Warp 0 scans the tile's
+// n_events, publishes the tile aggregate and walks back over predecessor
+// tiles (tiles are taken in launch order through a ticket counter, so a
+// predecessor is always resident or finished); then warp w emits episode w
+// of the tile.  Replaces scan (3 launches) + emit (1 launch) by one.
+constexpr uint64_t kTileAgg = 1ull << 62, kTilePrefix = 2ull << 62;
+constexpr uint64_t kTileValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(1024)
+    k_scan_emit(const uint8_t* __restrict__ step_mask, const int64_t* __restrict__ rec_start,
+                const int32_t* __restrict__ n_rec, const tl_label* __restrict__ labels, int n_env,
+                int64_t* __restrict__ ev_off, uint8_t* __restrict__ ev_kind,
+                int32_t* __restrict__ ev_t, unsigned long long* tile_state) {
+  __shared__ int s_tile;
+  __shared__ int64_t s_off[32];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int n_tiles = (n_env + 31) / 32;
+  if (threadIdx.x == 0)
+    s_tile = (int)atomicAdd(reinterpret_cast<unsigned long long*>(tile_state + n_tiles), 1ull);
+  __syncthreads();
+  const int tile = s_tile;
+  if (warp == 0) {
+    const int e = tile * 32 + lane;
+    const int64_t cnt = e < n_env ? labels[e].n_events : 0;
+    int64_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t u = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += u;
+    }
+    const int64_t total = __shfl_sync(kFull, incl, 31);
+    int64_t prefix = 0;
+    if (lane == 0) {
+      volatile unsigned long long* st = tile_state;
+      if (tile == 0) {
+        atomicExch(tile_state, kTilePrefix | (unsigned long long)total);
+      } else {
+        atomicExch(tile_state + tile, kTileAgg | (unsigned long long)total);
+        for (int t = tile - 1; t >= 0;) {
+          const unsigned long long v = st[t];
+          const unsigned long long flag = v & ~kTileValMask;
+          if (!flag) continue;  // predecessor not published yet
+          prefix += (int64_t)(v & kTileValMask);
+          if (flag == kTilePrefix) break;
+          t--;
+        }
+        atomicExch(tile_state + tile, kTilePrefix | (unsigned long long)(prefix + total));
+      }
+    }
+    prefix = __shfl_sync(kFull, prefix, 0);
+    const int64_t off = prefix + incl - cnt;
+    s_off[lane] = off;
+    if (e < n_env) ev_off[e] = off;
+    if (e == n_env - 1) ev_off[n_env] = off + cnt;
+  }
+  __syncthreads();
+  const int e = tile * 32 + warp;
+  if (e >= n_env || labels[e].n_events == 0) return;
+  const int sub = labels[e].subtask;
+  const int64_t rs = rec_start[e];
+  const int n = n_rec[e];
+  int64_t base = s_off[warp];
+  for (int t0 = 0; t0 < n; t0 += 32) {
+    const int t = t0 + lane;
+    const uint32_t mask = t < n ? step_mask[rs + t] : 0u;
+    const int cnt = __popc(mask);
+    const int incl = warp_incl_scan(cnt);
+    int64_t pos = base + incl - cnt;
+    uint32_t m = mask;
+    while (m) {
+      const int k = __ffs(m) - 1;
+      m &= m - 1;
+      ev_kind[pos] = kAlpha[sub][k];
+      ev_t[pos] = t;
+      pos++;
+    }
+    base += __shfl_sync(kFull, incl, 31);
+  }
+}
+
+}  // namespace tl

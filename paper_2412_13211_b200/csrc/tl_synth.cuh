@@ -43,6 +43,7 @@ struct SynthWarp {
   int32_t hw[kMaxSteps + 1];    // words per hold record in segment s
   StepSt st[kMaxSteps + 1];
   double dist_after[kMaxSteps];
+  double radv[32];
   uint8_t kind[kMaxSteps];
   uint8_t sflag[kMaxSteps];     // bit0 dist draw at the event
   int32_t misc[16];
@@ -657,47 +658,59 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
         // :210-213), run in lockstep by all lanes on shuffled draws (cum is
         // warp-uniform).  uniform(0.0, b) = RN(b * r) exactly for b, r >= 0.
         const int cnt = min(32, r_end - r0);
-        const unsigned adv_m = __ballot_sync(kFull, valid && adv);
-        const unsigned exc_m = __ballot_sync(
-            kFull, valid && ev == TL_EV_EXCESSIVE_COLLISIONS && !(perr && s == pstep));
-        float my_cum32 = 0.f;
+        const bool my_exc = valid && ev == TL_EV_EXCESSIVE_COLLISIONS && !(perr && s == pstep);
+        // draw (or -1: no draw, or -2: jump to 1.05*limit) broadcast via smem
+        S.radv[lane] = my_exc ? -2.0 : (valid && adv ? my_radv : -1.0);
+        __syncwarp();
+        double my_cum = 0.0;
+#pragma unroll 4
         for (int j = 0; j < cnt; j++) {
-          const double rj = __shfl_sync(kFull, my_radv, j);
-          if ((adv_m >> j) & 1u)
-            cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rj));
-          if ((exc_m >> j) & 1u) cum = z.L105;
-          if (lane == j) my_cum32 = __double2float_rn(cum);
+          const double rj = S.radv[j];
+          const double nxt = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rj));
+          cum = rj >= 0.0 ? nxt : (rj < -1.5 ? z.L105 : cum);
+          my_cum = lane == j ? cum : my_cum;
         }
+        const float my_cum32 = __double2float_rn(my_cum);
+        __syncwarp();
         // ---- emit + write + label ---------------------------------------------
         RecV<float> v;
         uint32_t ind = 0, errb = 0;
         if (valid) {
           const int64_t rr = rs + r;
           const StepSt stv = S.st[sidx];
-          const int eo = o + 2 * adv + 2 * app;
+          const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
+          float* __restrict__ dst = P + rr;  // plane f at dst + f*stride
+          // emitted draws in source order (synth.py:178-185); at rest: zeros
+          auto draw = [&](uint32_t k, double a, double b) -> float {
+            if (!emit) return 0.f;
+            const uint2 wv = ring2[((eo + 2u * k) & kRingMask) >> 1];
+            return __double2float_rn(uniform_rn(a, b, rand53(wv.x, wv.y)));
+          };
           float mq = 0.f, mqd = 0.f;
 #pragma unroll
           for (int i = 0; i < DOFMAX; i++) {
             if (i < dof) {
-              const float q = emit ? __double2float_rn(uniform_rn(-0.3, 0.3, rnd(eo + 2 * i))) : 0.f;
-              P[i * stride + rr] = q;
+              const float q = draw(i, -0.3, 0.3);
+              *dst = q;
+              dst += stride;
               mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
             }
           }
 #pragma unroll
           for (int i = 0; i < DOFMAX; i++) {
             if (i < dof) {
-              const float qd = emit ? __double2float_rn(uniform_rn(-0.4, 0.4, rnd(eo + 2 * (dof + i)))) : 0.f;
-              P[(dof + i) * stride + rr] = qd;
+              const float qd = draw(dof + i, -0.4, 0.4);
+              *dst = qd;
+              dst += stride;
               mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
             }
           }
-          const int eb2 = eo + 4 * dof;
-          v.tor = emit ? __double2float_rn(uniform_rn(-0.05, 0.05, rnd(eb2))) : 0.f;
-          v.vx = emit ? __double2float_rn(uniform_rn(-0.2, 0.2, rnd(eb2 + 2))) : 0.f;
-          v.vy = emit ? __double2float_rn(uniform_rn(-0.2, 0.2, rnd(eb2 + 4))) : 0.f;
-          v.om = emit ? __double2float_rn(uniform_rn(-0.3, 0.3, rnd(eb2 + 6))) : 0.f;
-          v.der = emit ? __double2float_rn(uniform_rn(0.2, 1.0, rnd(eb2 + 8))) : 0.f;
+          const uint32_t k2 = 2 * dof;
+          v.tor = draw(k2, -0.05, 0.05);
+          v.vx = draw(k2 + 1, -0.2, 0.2);
+          v.vy = draw(k2 + 2, -0.2, 0.2);
+          v.om = draw(k2 + 3, -0.3, 0.3);
+          v.der = draw(k2 + 4, 0.2, 1.0);
           v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
           v.force = stv.force;
           v.cum = my_cum32;
@@ -706,16 +719,15 @@ __global__ void __launch_bounds__(kSynthWarps * 32)
           v.qdm = mqd;
           v.jm = mq;
           v.jm_d = 0.0;
-          const int f0 = 2 * dof;
-          P[f0 * stride + rr] = v.tor;
-          P[(f0 + 1) * stride + rr] = v.vx;
-          P[(f0 + 2) * stride + rr] = v.vy;
-          P[(f0 + 3) * stride + rr] = v.om;
-          P[(f0 + 4) * stride + rr] = v.der;
-          P[(f0 + 5) * stride + rr] = v.dist;
-          P[(f0 + 6) * stride + rr] = v.force;
-          P[(f0 + 7) * stride + rr] = v.cum;
-          P[(f0 + 8) * stride + rr] = v.art;
+          dst[0] = v.tor;
+          dst[stride] = v.vx;
+          dst[2 * stride] = v.vy;
+          dst[3 * stride] = v.om;
+          dst[4 * stride] = v.der;
+          dst[5 * stride] = v.dist;
+          dst[6 * stride] = v.force;
+          dst[7 * stride] = v.cum;
+          dst[8 * stride] = v.art;
           p.out.grasped[rr] = (uint8_t)v.g;
           record_bits(c, v, sc_ru, sc_d, ind, errb);
         }

@@ -184,7 +184,26 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
 
 size_t tl_scan_scratch_bytes(int32_t n) {
   const size_t tiles = ((size_t)(n > 0 ? n : 1) + kScanBlock - 1) / kScanBlock;
-  return tiles * sizeof(int64_t);
+  const size_t tiles32 = ((size_t)(n > 0 ? n : 1) + 31) / 32 + 1;
+  return (tiles > tiles32 ? tiles : tiles32) * sizeof(int64_t);
+}
+
+int tl_scan_emit_events(const uint8_t* step_mask, const int64_t* rec_start, const int32_t* n_rec,
+                        const tl_label* labels, int32_t n_env, int64_t* ev_off, uint8_t* ev_kind,
+                        int32_t* ev_t, void* scratch, void* stream) {
+  if (!ev_off || n_env < 0 || (n_env > 0 && (!step_mask || !rec_start || !n_rec || !labels ||
+                                             !ev_kind || !ev_t || !scratch)))
+    return TL_E_INVALID;
+  if (n_env == 0) {
+    cudaMemsetAsync(ev_off, 0, sizeof(int64_t), S(stream));
+    return check_launch();
+  }
+  const int tiles = (n_env + 31) / 32;
+  cudaMemsetAsync(scratch, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), S(stream));
+  k_scan_emit<<<tiles, 1024, 0, S(stream)>>>(step_mask, rec_start, n_rec, labels, n_env, ev_off,
+                                              ev_kind, ev_t,
+                                              reinterpret_cast<unsigned long long*>(scratch));
+  return check_launch();
 }
 
 int tl_scan_events(const tl_label* labels, int32_t n, int64_t* ev_off, void* scratch, void* stream) {

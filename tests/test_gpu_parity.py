@@ -325,3 +325,21 @@ def test_mode_histogram(C, TH):
     h = C.mode_histogram(sb.labels, 3000).cpu().numpy()
     lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
     assert np.array_equal(h, np.bincount(lab["mode"], minlength=39))
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_fused_scan_emit_matches_two_pass(C, TH, kind):
+    """tl_scan_emit_events (decoupled look-back) == tl_scan_events + tl_emit_events."""
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_gap=64, max_tail=64)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 5000  # 157 tiles of 32 episodes
+    sb = C.fuzz_batch(np.arange(n) + 777, kind, cfg, TH(), cs)
+    a = C.LabelResult(sb.labels, sb.step_mask, None)
+    C.emit_events(sb.records, a)
+    b = C.LabelResult(sb.labels, sb.step_mask, None)
+    C.emit_events(sb.records, b, ev_capacity=n * C.fuzz_capacity(cfg))
+    assert torch.equal(a.ev_off, b.ev_off)
+    tot = int(a.ev_off[-1])
+    assert torch.equal(a.ev_kind[:tot], b.ev_kind[:tot])
+    assert torch.equal(a.ev_t[:tot], b.ev_t[:tot])
