@@ -168,6 +168,67 @@ def run_reference(args, rank, world):
     print(json.dumps(out))
 
 
+def label_sizing_run(L, core, lib, dev, stream, flush, n_env=1 << 19, reps=5):
+    """HBM roofline of the labelling kernel: 2^19 Pick episodes x 200 steps
+    (C1/C8 shape, 1.05e8 env steps, 9.8 GB of f32 planes), records resident
+    in HBM (far larger than L2).  One 4096-episode tile is realized on the
+    GPU and replicated; K1 reads only the fields Pick predicates need."""
+    import ctypes
+    import torch
+    from paper_2412_13211_b200.synth import EventScript, ScriptStep
+    from paper_2412_13211_b200.events import EventKind as E
+    from paper_2412_13211_b200.thresholds import Thresholds
+    from paper_2412_13211_b200 import _lib
+    tile = 4096
+    T = 200
+    arr = np.zeros(tile, _lib.SCRIPT_DTYPE)
+    kinds = np.tile(np.array([0, 1, 12], np.uint8), tile)   # Contact, Grasped, Success
+    gaps = np.full(3 * tile, 60, np.int32)
+    for i in range(tile):
+        arr[i] = (3 * i, i, 3, 19, 0, 0, 0, 0, 0, 7, 0.5)
+    cs12 = core.synth_csets(Thresholds()).to_device(dev)
+    sb = core.realize_batch(arr, kinds, gaps, Thresholds(), cs12)
+    R = n_env * T
+    planes = torch.empty((23, R), dtype=torch.float32, device=dev)
+    grasped = torch.empty(R, dtype=torch.uint8, device=dev)
+    reps_n = n_env // tile
+    planes.view(23, reps_n, tile * T).copy_(sb.records.planes[:, :tile * T].unsqueeze(1).expand(23, reps_n, tile * T))
+    grasped.view(reps_n, tile * T).copy_(sb.records.grasped[:tile * T].unsqueeze(0).expand(reps_n, tile * T))
+    rec_start = torch.arange(n_env, dtype=torch.int64, device=dev) * T
+    n_rec = torch.full((n_env,), T, dtype=torch.int32, device=dev)
+    rb = core.RecordBatch(planes, grasped, rec_start, n_rec, 7)
+    env = torch.zeros(n_env, dtype=torch.int32, device=dev)     # cset 0 = Pick
+    labels = torch.empty((n_env, 24), dtype=torch.uint8, device=dev)
+    mask = torch.empty(R, dtype=torch.uint8, device=dev)
+    rbc = rb.c()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    ms = []
+    for k in range(reps + 2):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        L.check(lib.tl_label_records(ctypes.byref(rbc), n_env, L.ptr(env), L.ptr(cs12), 12, None,
+                                     L.ptr(mask), None, L.ptr(labels), sp), "label")
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k >= 2:
+            ms.append(a.elapsed_time(b))
+    lab = labels.cpu().numpy().reshape(-1).view(_lib.LABEL_DTYPE)
+    assert (lab["status"] == 0).all() and (lab["mode"] == 0).all()  # pick.s1 everywhere
+    t = sum(ms) / len(ms) / 1e3
+    read_b = 81.0 * R        # Pick: q 28 + qd 28 + v 8 + w 4 + dist_ee_rest 4 + cum 4 + force 4 + grasped 1
+    write_b = 1.0 * R + 24.0 * n_env
+    hbm, _ = peaks()
+    del planes, grasped, mask
+    return {"kernel": "k_label<float,7> (tl_label_records)", "episodes": n_env,
+            "env_steps": R, "avg_launch_ms": 1e3 * t,
+            "env_steps_per_s": R / t, "trajectories_per_s": n_env / t,
+            "algorithmic_bytes_per_launch": read_b + write_b,
+            "achieved_GBps": (read_b + write_b) / t / 1e9, "peak_GBps": hbm,
+            "frac": (read_b + write_b) / t / 1e9 / hbm,
+            "note": "81 B/env-step read (Pick fields) + 1 B step mask + 24 B/episode label"}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -343,6 +404,8 @@ def main():
 
         t_e2e, e2e_recs, h2d_b, d2h_b = e2e_loop(False)
         t_e2r, e2r_recs, _, d2h_rb = e2e_loop(True)
+        # ---- sizing run: k_label over 2^19 x 200-step episodes
+        sizing = label_sizing_run(L, core, lib, dev, stream, flush)
     clk = clocks.summary()
 
     recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
@@ -403,6 +466,7 @@ def main():
                                  "d2h_bytes_per_step": d2h_rb,
                                  "note": "same, plus tl_compact_records + D2H of every "
                                          "generated record (93 B/env-step)"}},
+        "label_sizing": sizing,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
                          "sample": cb_sample, "trajectories_per_sec": cb_eps},
         "clocks": clk,

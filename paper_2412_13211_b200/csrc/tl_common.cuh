@@ -17,6 +17,14 @@
 
 namespace tl {
 
+#ifdef TL_PROFILE
+// phase timestamps of one CTA/warp (profiling build only, scripts/phase_probe.py)
+__device__ unsigned long long g_tl_prof[128];
+#define TL_STAMP(i) do { if (blockIdx.x == 0) g_tl_prof[(i)] = clock64(); } while (0)
+#else
+#define TL_STAMP(i) do { } while (0)
+#endif
+
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMtN = 624;
@@ -47,13 +55,20 @@ __device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t
   uint32_t v1 = (kTlInitGenrand[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + k0;
   mt[1] = v1;
   prev = v1;
-#pragma unroll 8
-  for (int i = 2; i < kMtN; i++) {
-    const int j = KLEN == 1 ? 0 : ((i - 1) & 1);
-    const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
-    const uint32_t v = (kTlInitGenrand[i] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
-    mt[i] = v;
-    prev = v;
+  for (int i0 = 2; i0 < kMtN; i0 += 8) {
+    uint32_t tab[8];  // table values of the group, loaded off the serial chain
+#pragma unroll
+    for (int k = 0; k < 8; k++) tab[k] = i0 + k < kMtN ? kTlInitGenrand[i0 + k] : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int i = i0 + k;
+      if (i < kMtN) {
+        const int j = KLEN == 1 ? 0 : ((i - 1) & 1);
+        const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
+        prev = (tab[k] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
+        mt[i] = prev;
+      }
+    }
   }
   mt[0] = prev;
   {
@@ -62,12 +77,20 @@ __device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t
     prev = (v1 ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
     mt[1] = prev;
   }
-  // second loop: N-1 iterations, i = 2..623 then wrap to i = 1
-#pragma unroll 8
-  for (int i = 2; i < kMtN; i++) {
-    const uint32_t v = (mt[i] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
-    mt[i] = v;
-    prev = v;
+  // second loop: N-1 iterations, i = 2..623 then wrap to i = 1.  The loads
+  // of a group are issued before its stores so shared-memory latency stays
+  // off the serial chain.
+  for (int i0 = 2; i0 < kMtN; i0 += 8) {
+    uint32_t old[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) old[k] = (i0 + k < kMtN) ? mt[i0 + k] : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (i0 + k < kMtN) {
+        prev = (old[k] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i0 + k);
+        mt[i0 + k] = prev;
+      }
+    }
   }
   mt[0] = prev;
   mt[1] = (mt[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;

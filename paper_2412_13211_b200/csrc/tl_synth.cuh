@@ -398,23 +398,20 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
   const bool valid = e < p.n_env;
   uint32_t* row = rows + lane * kRowWords;
   const int ms = p.cfg.max_events + 4;
+  if (lane == 0) TL_STAMP(0);
   if (valid) {
     const int64_t seed = p.seeds[e];
     mt_seed_lane(row, (lane & 1) ? (seed ^ 0x5EED) : seed);
+    if (lane == 0) TL_STAMP(1);
     if (!(lane & 1)) {
       MtLane R{row, 0};
       tl_script t;
       uint8_t* sk = p.step_kind + e * ms;
       int32_t* sg = p.step_gap + e * ms;
-      uint8_t k8[kMaxSteps];
-      int32_t g32[kMaxSteps];
-      const int ns = sample_script(R, p.fuzz_subtask, p.cfg, k8, g32, t);
+      // at most max_events + 4 = ms steps are ever produced (synth.py:463-505)
+      const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t);
       int64_t nr = 1;
-      for (int i = 0; i < (ns < 0 ? 0 : ns); i++) {
-        sk[i] = k8[i];
-        sg[i] = g32[i];
-        nr += g32[i];
-      }
+      for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += sg[i];
       const int64_t tmin = ns > 0 ? 0 : 1;
       nr += t.tail > tmin ? t.tail : tmin;
       if (nr < 2) nr = 2;
@@ -426,8 +423,10 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
       p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;
     }
   }
+  if (lane == 0) TL_STAMP(2);
   __syncwarp();
   copy_rows_out(rows, 1, 2, 16, p.states, e0, p.n_env);
+  if (lane == 0) TL_STAMP(3);
 }
 
 // realize path: seed the realize RNG of given scripts (one thread per state)

@@ -1,0 +1,458 @@
+// tl_synth_cta.cuh -- realize + online labelling with one 4-warp CTA per
+// episode (the latency-optimised form of k_synth).
+//
+// Same semantics as k_synth (tl_synth.cuh; reference synth.py:100-348 +
+// events.py:94-193 + modes.py:235-253), different mapping:
+//   * MT19937 block regeneration is spread over 64 threads: 10 iterations
+//     with ONE barrier each, because word i >= 227 reads word i-227, which
+//     is at least two iterations old, and word i < 227 reads old words;
+//   * a wave of 64 records is emitted at once, one record per thread, from
+//     a 16 KB ring of tempered words (small enough that all episodes of a
+//     1024-env batch are resident at once: ~23 KB shared memory per CTA);
+//   * the serial f64 cum_robot_force recurrence runs on warp 0, eight
+//     records per group of vector shared-memory loads, split at the
+//     ExcessiveCollisions record (before it every step draws, after it cum
+//     is constant);
+//   * each warp folds its 32 event masks into a partial label state,
+//     combined in order by warp 0.
+#pragma once
+#include "tl_synth.cuh"
+
+namespace tl {
+
+constexpr int kCtaThreads = 64;
+
+template <int DOFMAX>
+struct CtaCfg {
+  static constexpr int kRing = DOFMAX <= 7 ? 4096 : 8192;  // >= 64*(4+2*(2*DOFMAX+5)) + 623
+  static constexpr uint32_t kMask = kRing - 1;
+};
+
+template <int DOFMAX>
+struct CtaSmem {
+  uint32_t mt[kMtN];
+  uint32_t wb[CtaCfg<DOFMAX>::kRing];
+  int32_t gap[kMaxSteps];
+  int32_t tau[kMaxSteps];
+  int32_t W[kMaxSteps + 1];
+  int32_t hw[kMaxSteps + 1];
+  StepSt st[kMaxSteps + 1];
+  double dist_after[kMaxSteps];
+  double radv[kCtaThreads];
+  float cum32[kCtaThreads];
+  uint32_t ind[kCtaThreads];
+  uint32_t emask[kCtaThreads];
+  uint32_t eerr[kCtaThreads];
+  LState part[kCtaThreads / 32];
+  uint8_t kind[kMaxSteps];
+  uint8_t sflag[kMaxSteps];
+  int32_t misc[16];
+  int32_t red[8];
+  tl_cset cs;
+};
+
+template <int DOFMAX>
+__device__ __forceinline__ void mt_twist_block(uint32_t* mt, uint32_t* ring, uint32_t base) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int it = 0; it < 10; it++) {
+    const int i = it * kCtaThreads + t;
+    const bool ok = i < kMtN;
+    uint32_t nv = 0;
+    if (ok) {
+      const int i1 = i + 1 == kMtN ? 0 : i + 1;
+      const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);
+      nv = mt_mix(mt[i], mt[i1], mt[src]);
+    }
+    __syncthreads();
+    if (ok) {
+      mt[i] = nv;
+      ring[(base + (uint32_t)i) & CtaCfg<DOFMAX>::kMask] = mt_temper(nv);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int block_max2(int v, int32_t* red) {
+  const int warp = threadIdx.x >> 5;
+  v = __reduce_max_sync(kFull, v);
+  if (lane_id() == 0) red[warp] = v;
+  __syncthreads();
+  const int m = max(red[0], red[1]);
+  __syncthreads();
+  return m;
+}
+
+template <bool FUZZ, int DOFMAX>
+__global__ void __launch_bounds__(kCtaThreads)
+    k_synth_cta(SynthParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CtaSmem<DOFMAX>& S = *reinterpret_cast<CtaSmem<DOFMAX>*>(smem_raw);
+  constexpr uint32_t kMask = CtaCfg<DOFMAX>::kMask;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  const int dof = p.out.dof;
+  float* __restrict__ P = reinterpret_cast<float*>(p.out.planes);
+  const int64_t stride = p.out.plane_stride;
+  const float fnan = __int_as_float(0x7fc00000);
+  const uint2* ring2 = reinterpret_cast<const uint2*>(S.wb);
+
+  int wave_no = 0;
+  for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
+    if (tid == 0 && e == 0) TL_STAMP(10);
+    // ---------------- script + seeded RNG state -------------------------------
+    const tl_script sc = p.scripts[e];
+    const int64_t rs = p.out.rec_start[e];
+    const int n_rec = p.out.n_rec[e];
+    {
+      const uint32_t* src = p.states + (int64_t)e * kMtN;
+      for (int i = tid; i < kMtN; i += kCtaThreads) S.mt[i] = src[i];
+    }
+    if (FUZZ && sc.n_steps < 0) {
+      if (tid == 0) {
+        tl_label L;
+        L.status = TL_ERR_SCRIPT_CAPACITY; L.n_events = 0; L.err_index = -1;
+        L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
+        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
+        p.labels[e] = L;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
+    if (warp == 0) stage_cset(&S.cs, &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
+    RzConst z;
+    const int st0 = realizer_init(z, sc, p.th, dof);
+    __syncthreads();
+    auto fail = [&](int code, int step) {
+      if (tid == 0) {
+        tl_label L;
+        L.status = code; L.n_events = 0; L.err_index = step;
+        L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
+        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
+        p.labels[e] = L;
+        if (FUZZ) p.out.n_rec[e] = 0;
+      }
+    };
+    if (st0 != TL_OK) {
+      fail(st0, -1);
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0 && e == 0) TL_STAMP(11);
+    PlanSt ps;  // initial realizer state (synth.py:111-158)
+    ps.force = (z.has_force && sc.initial_contact) ? 1.2 : 0.0;
+    ps.grasped = sc.initial_grasped ? 1 : 0;
+    ps.at_rest = 0;
+    ps.exc = 0;
+    if (z.kind == TL_OPEN) {
+      ps.level = sc.initial_level;
+      ps.art = sc.initial_level == TL_LVL_LOW ? z.lv_low : sc.initial_level == TL_LVL_SLIGHT ? z.lv_slight : z.lv_open;
+    } else if (z.kind == TL_CLOSE) {
+      ps.level = sc.initial_level == TL_LVL_CLOSED ? TL_LVL_CLOSED : TL_LVL_OPEN;
+      ps.art = z.a_q0;
+    } else {
+      ps.level = TL_LVL_LOW;
+      ps.art = 0.0;
+    }
+    const double dist0 = z.has_goal ? sc.initial_dist_obj_goal : __longlong_as_double(0x7ff8000000000000ll);
+    const tl_cset& c = S.cs;
+    float sc_ru = 0.f;
+    double sc_d = 0.0;
+    if (c.subtask == TL_CLOSE) close_cut(c, (double)__double2float_rn(ps.art), sc_ru, sc_d);
+    const double d0 = (double)__double2float_rn(dist0);
+
+    LState LS;                 // live in warp 0
+    lstate_init(LS);
+    uint32_t ind_carry = 0;    // indicator bits of the previous wave's last record
+    double cum = 0.0;          // warp 0: serial f64 recurrence
+    double dist_carry = dist0;
+    int32_t w_carry = 2 * z.ne;
+    int32_t tau_prev = 0;
+    uint32_t produced = 0;
+    int err_code = 0, err_step = -1;
+    int s_base = 0;
+    const int n_steps = sc.n_steps;
+    PlanSt pcarry = ps;
+    bool first_window = true;
+    for (;;) {
+      const int ns = min(n_steps - s_base, kMaxSteps);
+      const bool last_window = s_base + ns >= n_steps;
+      for (int i = tid; i < ns; i += kCtaThreads) {
+        S.kind[i] = p.step_kind[sc.step_off + s_base + i];
+        S.gap[i] = p.step_gap[sc.step_off + s_base + i];
+      }
+      __syncthreads();
+      if (tid == 0) {  // plan: record/word layout + deterministic state
+        PlanSt q = pcarry;
+        int32_t w = w_carry, r = tau_prev;
+        int last_draw = -1, perr = 0, pstep = ns;
+        int exc_at = 0x7fffffff;  // record of the ExcessiveCollisions jump
+        S.st[0] = make_st(z, q, -1);
+        for (int s = 0; s < ns; s++) {
+          const int g = S.gap[s];
+          if (g < 1) { perr = TL_INF_GAP; pstep = s; S.W[s] = w; S.hw[s] = 0; S.tau[s] = r; break; }
+          S.W[s] = w;
+          const int hwv = (q.exc ? 0 : 2) + (q.at_rest ? 0 : 2 * z.ne);
+          S.hw[s] = hwv;
+          w += (g - 1) * hwv;
+          r += g;
+          S.tau[s] = r;
+          int wev = q.exc ? 0 : 2;
+          int draw = 0;
+          const int ec = plan_apply(z, q, S.kind[s], draw);
+          S.sflag[s] = (uint8_t)draw;
+          if (ec) { perr = ec; pstep = s; break; }
+          if (draw) last_draw = s;
+          if (S.kind[s] == TL_EV_EXCESSIVE_COLLISIONS) exc_at = r;
+          wev += (draw ? 2 : 0) + (q.at_rest ? 0 : 2 * z.ne);
+          w += wev;
+          S.st[s + 1] = make_st(z, q, last_draw);
+        }
+        S.misc[14] = pcarry.exc ? -1 : exc_at;
+        if (!perr) {
+          S.W[ns] = w;
+          S.hw[ns] = (q.exc ? 0 : 2) + (q.at_rest ? 0 : 2 * z.ne);
+        }
+        S.misc[0] = perr; S.misc[1] = pstep; S.misc[2] = w; S.misc[3] = r;
+        S.misc[4] = q.grasped; S.misc[5] = q.at_rest; S.misc[6] = q.exc; S.misc[7] = q.level;
+        reinterpret_cast<double*>(&S.misc[8])[0] = q.force;
+        reinterpret_cast<double*>(&S.misc[10])[0] = q.art;
+      }
+      __syncthreads();
+      if (tid == 0 && e == 0) TL_STAMP(12);
+      const int perr = S.misc[0], pstep = S.misc[1];
+      const int exc_rec = S.misc[14];
+      const int r_begin = first_window ? 0 : tau_prev + 1;
+      int r_end;
+      if (perr) r_end = S.tau[pstep] + 1;
+      else if (last_window) r_end = n_rec;
+      else r_end = S.misc[3] + 1;
+      int seg_hint = 0;
+      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += kCtaThreads) {
+        const int r = r0 + tid;
+        const bool valid = r < r_end;
+        int o = 0, adv = 0, app = 0, emit = 0, sidx = 0, ev = -1, s = 0;
+        if (valid) {
+          if (r == 0) {
+            emit = 1;
+          } else {
+            s = seg_hint;
+            while (s < ns && S.tau[s] < r) s++;
+            if (s < ns && S.tau[s] == r) {
+              o = S.W[s] + (S.gap[s] - 1) * S.hw[s];
+              adv = !S.st[s].exc;
+              ev = S.kind[s];
+              const bool failing = perr && s == pstep;
+              app = failing ? 0 : (S.sflag[s] & 1);
+              emit = failing ? 0 : !S.st[s + 1].at_rest;
+              sidx = failing ? s : s + 1;
+            } else {
+              const int first = (s == 0 ? tau_prev : S.tau[s - 1]) + 1;
+              o = S.W[s] + (r - first) * S.hw[s];
+              adv = !S.st[s].exc;
+              emit = !S.st[s].at_rest;
+              sidx = s;
+            }
+          }
+        }
+        if (tid == 0) S.misc[12] = s;
+        const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
+        const int need_max = block_max2(need, S.red);  // also publishes misc[12]
+        seg_hint = S.misc[12];
+        const int wbase = 20 + 8 * min(wave_no, 12);  // profiling build only
+        if (tid == 0 && e == 0) TL_STAMP(wbase);
+        while ((int)produced < need_max) {
+          mt_twist_block<DOFMAX>(S.mt, S.wb, produced);
+          produced += kMtN;
+        }
+        if (tid == 0 && e == 0) TL_STAMP(wbase + 1);
+        auto rnd = [&](int woff) {
+          const uint2 wv = ring2[((uint32_t)woff & kMask) >> 1];
+          return rand53(wv.x, wv.y);
+        };
+        int my_err = 0;
+        S.radv[tid] = valid && adv ? rnd(o) : 0.0;
+        if (valid && app) {
+          const double rr = rnd(o + 2 * adv);
+          S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rr) : uniform_rn(0.3, 0.8, rr);
+        }
+        if (tid == 0) S.misc[13] = 0x7fffffff;
+        __syncthreads();
+        if (tid == 0 && e == 0) TL_STAMP(wbase + 2);
+        double dist_rec = dist_carry;
+        if (valid && z.has_goal) {
+          const int ld = S.st[sidx].last_draw;
+          dist_rec = ld >= 0 ? S.dist_after[ld] : dist_carry;
+          if (ev >= 0) {
+            const int ldb = S.st[s].last_draw;
+            const double db = ldb >= 0 ? S.dist_after[ldb] : dist_carry;
+            switch (ev) {  // value-dependent checks of _apply (synth.py:218-260)
+              case TL_EV_OBJ_AT_GOAL: if (db <= z.goal) my_err = TL_INF_AT_GOAL_ALREADY; break;
+              case TL_EV_OBJ_LEFT_GOAL: if (db > z.goal) my_err = TL_INF_LEFT_NOT_AT_GOAL; break;
+              case TL_EV_RELEASED_AT_GOAL: if (db > z.goal) my_err = TL_INF_RAG; break;
+              case TL_EV_RELEASED_OUTSIDE_GOAL: if (db <= z.goal) my_err = TL_INF_ROG; break;
+              case TL_EV_SUCCESS: if (db > z.goal) my_err = TL_INF_SUCCESS_UNREACHABLE; break;
+            }
+          }
+        }
+        if (valid && perr && ev >= 0 && s == pstep && !my_err) my_err = perr;
+        if (my_err) atomicMin(&S.misc[13], ((s_base + s) << 8) | my_err);
+        const int cnt = min(kCtaThreads, r_end - r0);
+        // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213)
+        // on warp 0.  Record 0 never draws; every later record draws until
+        // the ExcessiveCollisions record, which jumps to 1.05*limit for good.
+        if (warp == 0) {
+          const int jx = exc_rec >= r0 ? min(cnt, exc_rec - r0) : 0;  // draws in [j0, jx)
+          int j = 0;
+          if (r0 == 0) {
+            if (lane == 0) S.cum32[0] = 0.f;
+            j = 1;
+          }
+          for (; j + 8 <= jx; j += 8) {
+            double rg[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) rg[k] = S.radv[j + k];
+            float out[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+              cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rg[k]));
+              out[k] = __double2float_rn(cum);
+            }
+            if (lane < 8) {
+              float v = out[0];
+#pragma unroll
+              for (int k = 1; k < 8; k++) v = lane == k ? out[k] : v;
+              S.cum32[j + lane] = v;
+            }
+          }
+          for (; j < jx; j++) {
+            cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), S.radv[j]));
+            if (lane == 0) S.cum32[j] = __double2float_rn(cum);
+          }
+          if (jx < cnt && r0 + cnt > exc_rec) {
+            cum = z.L105;
+            const float c105 = __double2float_rn(cum);
+            for (int k = max(j, 0) + lane; k < cnt; k += 32) S.cum32[k] = c105;
+          }
+        }
+        __syncthreads();
+        const int ek = S.misc[13];
+        if (ek != 0x7fffffff) {
+          err_code = ek & 0xff;
+          err_step = ek >> 8;
+          break;
+        }
+        // ---- emit + write + per-record indicator bits ----------------------------
+        uint32_t ind = 0, errb = 0;
+        if (valid) {
+          const int64_t rr = rs + r;
+          const StepSt stv = S.st[sidx];
+          const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
+          float* __restrict__ dst = P + rr;
+          auto draw = [&](uint32_t k, double a, double b) -> float {
+            if (!emit) return 0.f;
+            const uint2 wv = ring2[((eo + 2u * k) & kMask) >> 1];
+            return __double2float_rn(uniform_rn(a, b, rand53(wv.x, wv.y)));
+          };
+          RecV<float> v;
+          float mq = 0.f, mqd = 0.f;
+#pragma unroll
+          for (int i = 0; i < DOFMAX; i++) {
+            if (i < dof) {
+              const float q = draw(i, -0.3, 0.3);
+              *dst = q;
+              dst += stride;
+              mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < DOFMAX; i++) {
+            if (i < dof) {
+              const float qd = draw(dof + i, -0.4, 0.4);
+              *dst = qd;
+              dst += stride;
+              mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
+            }
+          }
+          const uint32_t k2 = 2 * dof;
+          v.tor = draw(k2, -0.05, 0.05);
+          v.vx = draw(k2 + 1, -0.2, 0.2);
+          v.vy = draw(k2 + 2, -0.2, 0.2);
+          v.om = draw(k2 + 3, -0.3, 0.3);
+          v.der = draw(k2 + 4, 0.2, 1.0);
+          v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
+          v.force = stv.force;
+          v.cum = S.cum32[tid];
+          v.art = stv.art;
+          v.g = stv.grasped != 0;
+          v.qdm = mqd;
+          v.jm = mq;
+          v.jm_d = 0.0;
+          dst[0] = v.tor;
+          dst[stride] = v.vx;
+          dst[2 * stride] = v.vy;
+          dst[3 * stride] = v.om;
+          dst[4 * stride] = v.der;
+          dst[5 * stride] = v.dist;
+          dst[6 * stride] = v.force;
+          dst[7 * stride] = v.cum;
+          dst[8 * stride] = v.art;
+          p.out.grasped[rr] = (uint8_t)v.g;
+          record_bits(c, v, sc_ru, sc_d, ind, errb);
+        }
+        S.ind[tid] = ind;
+        __syncthreads();
+        if (tid == 0 && e == 0) TL_STAMP(wbase + 4);
+        const uint32_t prev = tid ? S.ind[tid - 1] : ind_carry;
+        const uint32_t mask = (valid && r > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
+        if (valid && p.step_mask) p.step_mask[rs + r] = (uint8_t)mask;
+        ind_carry = S.ind[cnt - 1];
+        {  // per-warp partial fold, combined in record order by warp 0
+          LState part;
+          lstate_init(part);
+          lstate_fold(part, mask, valid ? errb : 0u);
+          if (lane == 0) S.part[warp] = part;
+        }
+        __syncthreads();
+        if (warp == 0) {
+#pragma unroll
+          for (int w = 0; w < kCtaThreads / 32; w++) {
+            const LState& q = S.part[w];
+#pragma unroll
+            for (int k = 0; k < 7; k++)
+              if (q.last[k] >= 0) LS.last[k] = LS.size + q.last[k];
+            LS.size += q.size;
+            LS.err_any |= q.err_any;
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && e == 0) TL_STAMP(wbase + 5);
+        if (e == 0) wave_no++;
+      }
+      if (!err_code && perr) { err_code = perr; err_step = s_base + pstep; }
+      if (err_code || last_window) break;
+      {
+        const int ld = S.st[ns].last_draw;
+        if (ld >= 0) dist_carry = S.dist_after[ld];
+      }
+      pcarry.grasped = S.misc[4]; pcarry.at_rest = S.misc[5]; pcarry.exc = S.misc[6]; pcarry.level = S.misc[7];
+      pcarry.force = reinterpret_cast<const double*>(&S.misc[8])[0];
+      pcarry.art = reinterpret_cast<const double*>(&S.misc[10])[0];
+      w_carry = S.misc[2];
+      tau_prev = S.misc[3];
+      s_base += ns;
+      first_window = false;
+      __syncthreads();
+    }
+    if (err_code) {
+      fail(err_code, err_step);
+    } else if (warp == 0) {
+      finish_label(c, LS, d0, p.rules, &p.labels[e]);
+    }
+    __syncthreads();
+    if (tid == 0 && e == 0) TL_STAMP(13);
+    if (tid == 0 && e == gridDim.x) TL_STAMP(14);
+  }
+}
+
+}  // namespace tl

@@ -8,6 +8,7 @@
 #include "tl_common.cuh"
 #include "tl_label.cuh"
 #include "tl_synth.cuh"
+#include "tl_synth_cta.cuh"
 #include "tl_filter.cuh"
 
 namespace {
@@ -251,16 +252,17 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
     set_max_smem(k_seed_states, rows_smem);
     k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
   }
-  const int smem = kSynthWarps * (int)sizeof(SynthWarp);
+  // realize + label: one 4-warp CTA per episode (tl_synth_cta.cuh)
   const bool small = sp.out.dof <= 7;
-  void (*k)(SynthParams) = fuzz ? (small ? k_synth<true, 7> : k_synth<true, 16>)
-                                : (small ? k_synth<false, 7> : k_synth<false, 16>);
+  const int smem = small ? (int)sizeof(CtaSmem<7>) : (int)sizeof(CtaSmem<16>);
+  void (*k)(SynthParams) = fuzz ? (small ? k_synth_cta<true, 7> : k_synth_cta<true, 16>)
+                                : (small ? k_synth_cta<false, 7> : k_synth_cta<false, 16>);
   set_max_smem(k, smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSynthWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCtaThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int grid = blocks_for(sp.n_env, kSynthWarps, sm_count() * per_sm);
-  k<<<grid, kSynthWarps * 32, smem, S(stream)>>>(sp);
+  const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
+  k<<<grid, kCtaThreads, smem, S(stream)>>>(sp);
   return check_launch();
 }
 
@@ -421,6 +423,12 @@ int tl_compact_records(const tl_records* src, int32_t n_env, const int64_t* dst_
   else k_compact<double><<<grid, 256, 0, S(stream)>>>(*src, n_env, dst_start, *dst, np_);
   return check_launch();
 }
+
+#ifdef TL_PROFILE
+int tl_prof_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tl_prof, sizeof(unsigned long long) * 128) == cudaSuccess ? 0 : TL_E_CUDA;
+}
+#endif
 
 int tl_mode_histogram(const tl_label* labels, int32_t n, int64_t* hist, void* stream) {
   if (!hist || n < 0 || (n > 0 && !labels)) return TL_E_INVALID;
