@@ -48,60 +48,74 @@ __device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t src)
 // random.Random(int) seeding of one state (one thread; init_by_array of
 // Modules/_randommodule.c).  key = abs(seed) as little-endian 32-bit words
 // (1 or 2 words for |seed| < 2^64).  `mt` may be a padded shared-memory row.
+// `out` (optional) receives the final state (e.g. a global-memory copy);
+// `mt` is the working row (the second loop reads the first loop's values).
+// Groups of 8 with exact bounds (622 = 77*8 + 6): no predication, the
+// table constants of a group are loaded before its serial chain.
 template <int KLEN>
-__device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t k1) {
-  uint32_t prev = kTlInitGenrand[0];
-  // first loop, k = max(624, klen) = 624 iterations: i = 1..623, then i = 1
-  uint32_t v1 = (kTlInitGenrand[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + k0;
-  mt[1] = v1;
-  prev = v1;
-  for (int i0 = 2; i0 < kMtN; i0 += 8) {
-    uint32_t tab[8];  // table values of the group, loaded off the serial chain
-#pragma unroll
-    for (int k = 0; k < 8; k++) tab[k] = i0 + k < kMtN ? kTlInitGenrand[i0 + k] : 0u;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int i = i0 + k;
-      if (i < kMtN) {
-        const int j = KLEN == 1 ? 0 : ((i - 1) & 1);
-        const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
-        prev = (tab[k] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
-        mt[i] = prev;
-      }
-    }
-  }
-  mt[0] = prev;
-  {
-    const int j = KLEN == 1 ? 0 : ((kMtN - 1) & 1);  // 624th iteration: j = 623 % klen
-    const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
-    prev = (v1 ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
-    mt[1] = prev;
-  }
-  // second loop: N-1 iterations, i = 2..623 then wrap to i = 1.  The loads
-  // of a group are issued before its stores so shared-memory latency stays
-  // off the serial chain.
-  for (int i0 = 2; i0 < kMtN; i0 += 8) {
-    uint32_t old[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) old[k] = (i0 + k < kMtN) ? mt[i0 + k] : 0u;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      if (i0 + k < kMtN) {
-        prev = (old[k] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i0 + k);
-        mt[i0 + k] = prev;
-      }
-    }
-  }
-  mt[0] = prev;
-  mt[1] = (mt[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
-  mt[0] = 0x80000000u;
+__device__ __forceinline__ uint32_t seed_step1(uint32_t prev, uint32_t tab, int i, uint32_t k0,
+                                               uint32_t k1) {
+  const int j = KLEN == 1 ? 0 : ((i - 1) & 1);
+  const uint32_t key = KLEN == 1 ? k0 : (j ? k1 + 1u : k0);
+  return (tab ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
 }
 
-__device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed) {
+template <int KLEN>
+__device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t k1,
+                                             uint32_t* out) {
+  uint32_t prev = kTlInitGenrand[0];
+  // first loop, k = max(624, klen) = 624 iterations: i = 1..623, then i = 1
+  const uint32_t v1 = seed_step1<KLEN>(prev, kTlInitGenrand[1], 1, k0, k1);
+  mt[1] = v1;
+  prev = v1;
+  int i0 = 2;
+  for (; i0 + 8 <= kMtN; i0 += 8) {
+    uint32_t tab[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) tab[k] = kTlInitGenrand[i0 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      prev = seed_step1<KLEN>(prev, tab[k], i0 + k, k0, k1);
+      mt[i0 + k] = prev;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < (kMtN - 2) % 8; k++) {
+    prev = seed_step1<KLEN>(prev, kTlInitGenrand[i0 + k], i0 + k, k0, k1);
+    mt[i0 + k] = prev;
+  }
+  mt[0] = prev;
+  prev = seed_step1<KLEN>(prev, v1, kMtN, k0, k1);  // 624th iteration: i = 1, j = 623 % klen
+  mt[1] = prev;
+  // second loop: N-1 iterations, i = 2..623 then wrap to i = 1
+  i0 = 2;
+  for (; i0 + 8 <= kMtN; i0 += 8) {
+    uint32_t old[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) old[k] = mt[i0 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      prev = (old[k] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i0 + k);
+      out[i0 + k] = prev;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < (kMtN - 2) % 8; k++) {
+    prev = (mt[i0 + k] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i0 + k);
+    out[i0 + k] = prev;
+  }
+  const uint32_t m1 = (mt[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
+  out[1] = m1;
+  out[0] = 0x80000000u;
+}
+
+// seed one state; the result lands in `out` (== mt for an in-place seed)
+__device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed, uint32_t* out = nullptr) {
   const uint64_t n = seed < 0 ? (uint64_t)0 - (uint64_t)seed : (uint64_t)seed;
   const uint32_t k0 = (uint32_t)n, k1 = (uint32_t)(n >> 32);
-  if (k1) mt_seed_impl<2>(mt, k0, k1);
-  else mt_seed_impl<1>(mt, k0, 0u);
+  if (!out) out = mt;
+  if (k1) mt_seed_impl<2>(mt, k0, k1, out);
+  else mt_seed_impl<1>(mt, k0, 0u, out);
 }
 
 // Warp-cooperative regeneration of all 624 words in place (CPython's
@@ -160,7 +174,22 @@ __device__ __forceinline__ void mt_twist_warp(uint32_t* mt, uint32_t* ring,
 struct MtLane {
   uint32_t* mt;
   int idx;  // next word of the current block (0 right after seeding)
+  int pre;  // words [0, pre) of the first block are already regenerated in place
+  // regenerate words [0, n) (n <= 227: they read old words only) with
+  // independent loads, so the serial sampler only tempers them
+  __device__ __forceinline__ void prepare(int n) {
+    for (int i0 = 0; i0 < n; i0 += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] = mt_mix(mt[i0 + k], mt[i0 + k + 1], mt[i0 + k + kMtM]);
+#pragma unroll
+      for (int k = 0; k < 8; k++) mt[i0 + k] = v[k];
+    }
+    pre = n;
+  }
   __device__ __forceinline__ uint32_t genrand() {
+    if (idx < pre) return mt_temper(mt[idx++]);
+    pre = 0;  // first block prefix consumed; continue lazily
     const int i = idx;
     const int i1 = i + 1 == kMtN ? 0 : i + 1;
     const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);

@@ -378,33 +378,28 @@ __device__ __forceinline__ StepSt make_st(const RzConst& z, const PlanSt& p, int
 // random_script; odd lanes seed the realize RNG (seed ^ 0x5EED, synth.py:515).
 constexpr int kRowWords = kMtN + 1;
 
-__device__ __forceinline__ void copy_rows_out(const uint32_t* rows, int first_row, int row_step,
-                                              int n_rows, uint32_t* dst, int64_t e0, int n_env) {
-  const int lane = lane_id();
-  for (int j = 0; j < n_rows; j++) {
-    const int64_t e = e0 + j;
-    if (e >= n_env) break;
-    const uint32_t* src = rows + (first_row + j * row_step) * kRowWords;
-    uint32_t* d = dst + e * kMtN;
-    for (int i = lane; i < kMtN; i += 32) d[i] = src[i];
-  }
-}
-
+// EPW episodes per warp: lanes 2j / 2j+1 own episode j (script RNG +
+// random_script / realize RNG).  EPW = 1 for small (latency-bound) batches:
+// sampling is serial branchy code, and 16 samplers in one warp diverge.
+template <int EPW>
 __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
-  extern __shared__ uint32_t rows[];  // [32][kRowWords]
+  extern __shared__ uint32_t rows[];  // [2*EPW][kRowWords]
   const int lane = lane_id();
-  const int64_t e0 = (int64_t)blockIdx.x * 16;
+  const int64_t e0 = (int64_t)blockIdx.x * EPW;
   const int64_t e = e0 + (lane >> 1);
-  const bool valid = e < p.n_env;
-  uint32_t* row = rows + lane * kRowWords;
+  const bool valid = (lane >> 1) < EPW && e < p.n_env;
+  uint32_t* row = rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
   const int ms = p.cfg.max_events + 4;
   if (lane == 0) TL_STAMP(0);
   if (valid) {
     const int64_t seed = p.seeds[e];
-    mt_seed_lane(row, (lane & 1) ? (seed ^ 0x5EED) : seed);
+    // odd lanes: realize RNG, final state written straight to global memory
+    mt_seed_lane(row, (lane & 1) ? (seed ^ 0x5EED) : seed,
+                 (lane & 1) ? p.states + e * kMtN : nullptr);
     if (lane == 0) TL_STAMP(1);
     if (!(lane & 1)) {
-      MtLane R{row, 0};
+      MtLane R{row, 0, 0};
+      R.prepare(128);
       tl_script t;
       uint8_t* sk = p.step_kind + e * ms;
       int32_t* sg = p.step_gap + e * ms;
@@ -424,9 +419,6 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
     }
   }
   if (lane == 0) TL_STAMP(2);
-  __syncwarp();
-  copy_rows_out(rows, 1, 2, 16, p.states, e0, p.n_env);
-  if (lane == 0) TL_STAMP(3);
 }
 
 // realize path: seed the realize RNG of given scripts (one thread per state)
@@ -435,9 +427,7 @@ __global__ void __launch_bounds__(32) k_seed_states(SynthParams p) {
   const int lane = lane_id();
   const int64_t e0 = (int64_t)blockIdx.x * 32;
   const int64_t e = e0 + lane;
-  if (e < p.n_env) mt_seed_lane(rows + lane * kRowWords, p.scripts[e].seed);
-  __syncwarp();
-  copy_rows_out(rows, 0, 1, 32, p.states, e0, p.n_env);
+  if (e < p.n_env) mt_seed_lane(rows + lane * kRowWords, p.scripts[e].seed, p.states + e * kMtN);
 }
 
 template <bool FUZZ, int DOFMAX>
