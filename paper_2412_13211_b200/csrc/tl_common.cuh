@@ -217,8 +217,14 @@ struct MtLane {
   }
 };
 
+// random() = k * 2^-53 for the 53-bit integer k; the exact conversion is
+// followed by an exponent decrement instead of a multiply (k >= 1 keeps the
+// result normal; k == 0 gives 0.0)
 __device__ __forceinline__ double rand53(uint32_t w0, uint32_t w1) {
-  return __ull2double_rn(((uint64_t)(w0 >> 5) << 26) | (w1 >> 6)) * 0x1.0p-53;
+  const uint64_t k = ((uint64_t)(w0 >> 5) << 26) | (w1 >> 6);
+  const double d = __ull2double_rn(k);
+  const double r = __longlong_as_double(__double_as_longlong(d) - (53ll << 52));
+  return k ? r : 0.0;
 }
 
 // Lib/random.py uniform: a + (b - a) * random(), no FMA

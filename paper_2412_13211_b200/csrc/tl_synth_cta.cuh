@@ -3,9 +3,8 @@
 //
 // Same semantics as k_synth (tl_synth.cuh; reference synth.py:100-348 +
 // events.py:94-193 + modes.py:235-253), different mapping:
-//   * MT19937 block regeneration is spread over 64 threads: 10 iterations
-//     with ONE barrier each, because word i >= 227 reads word i-227, which
-//     is at least two iterations old, and word i < 227 reads old words;
+//   * MT19937 block regeneration is spread over 64 threads in three phases
+//     of 4-word groups (6 barriers per block, 128-bit shared accesses);
 //   * a wave of 64 records is emitted at once, one record per thread, from
 //     a 16 KB ring of tempered words (small enough that all episodes of a
 //     1024-env batch are resident at once: ~23 KB shared memory per CTA);
@@ -51,26 +50,47 @@ struct CtaSmem {
   tl_cset cs;
 };
 
-template <int DOFMAX>
-__device__ __forceinline__ void mt_twist_block(uint32_t* mt, uint32_t* ring, uint32_t base) {
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int it = 0; it < 10; it++) {
-    const int i = it * kCtaThreads + t;
-    const bool ok = i < kMtN;
-    uint32_t nv = 0;
-    if (ok) {
-      const int i1 = i + 1 == kMtN ? 0 : i + 1;
-      const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);
-      nv = mt_mix(mt[i], mt[i1], mt[src]);
-    }
-    __syncthreads();
-    if (ok) {
-      mt[i] = nv;
-      ring[(base + (uint32_t)i) & CtaCfg<DOFMAX>::kMask] = mt_temper(nv);
-    }
+// CPython's block regeneration in 4-word groups (group g = words 4g..4g+3).
+// Word i reads words i+1 and i+397 (old, i < 227) or i-227 (new), i.e. a
+// group depends on groups 56-57 earlier, so three phases of <= 56 groups
+// (0..55 | 56..111 | 112..155) are each internally independent: one group
+// per thread (64 threads), 128-bit shared-memory loads/stores, every phase
+// loading before it stores (a group's i+1 neighbour is the next group's
+// first word) -> 6 barriers per 624-word block.
+template <int DOFMAX, int G0, int G1>
+__device__ __forceinline__ void twist_phase4(uint32_t* mt, uint32_t* ring, uint32_t base) {
+  static_assert(G1 - G0 <= kCtaThreads, "one group per thread");
+  const int g = G0 + threadIdx.x;
+  const bool ok = g < G1;
+  uint4 nv = make_uint4(0, 0, 0, 0);
+  if (ok) {
+    const uint4 cur = reinterpret_cast<const uint4*>(mt)[g];
+    const int i = 4 * g;
+    const uint32_t nxt = mt[i + 4 == kMtN ? 0 : i + 4];
+    auto src = [&](int k) {
+      const int ii = i + k;
+      return mt[ii < kMtN - kMtM ? ii + kMtM : ii - (kMtN - kMtM)];
+    };
+    const uint32_t s0 = src(0), s1 = src(1), s2 = src(2), s3 = src(3);
+    nv.x = mt_mix(cur.x, cur.y, s0);
+    nv.y = mt_mix(cur.y, cur.z, s1);
+    nv.z = mt_mix(cur.z, cur.w, s2);
+    nv.w = mt_mix(cur.w, nxt, s3);
   }
   __syncthreads();
+  if (ok) {
+    reinterpret_cast<uint4*>(mt)[g] = nv;
+    const uint4 tv = make_uint4(mt_temper(nv.x), mt_temper(nv.y), mt_temper(nv.z), mt_temper(nv.w));
+    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX>::kMask) >> 2] = tv;
+  }
+  __syncthreads();
+}
+
+template <int DOFMAX>
+__device__ __forceinline__ void mt_twist_block(uint32_t* mt, uint32_t* ring, uint32_t base) {
+  twist_phase4<DOFMAX, 0, 56>(mt, ring, base);
+  twist_phase4<DOFMAX, 56, 112>(mt, ring, base);
+  twist_phase4<DOFMAX, 112, 156>(mt, ring, base);
 }
 
 __device__ __forceinline__ int block_max2(int v, int32_t* red) {
@@ -318,11 +338,11 @@ __global__ void __launch_bounds__(kCtaThreads)
               cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rg[k]));
               out[k] = __double2float_rn(cum);
             }
-            if (lane < 8) {
-              float v = out[0];
-#pragma unroll
-              for (int k = 1; k < 8; k++) v = lane == k ? out[k] : v;
-              S.cum32[j + lane] = v;
+            if (lane == 0) {
+              S.cum32[j + 0] = out[0]; S.cum32[j + 1] = out[1];
+              S.cum32[j + 2] = out[2]; S.cum32[j + 3] = out[3];
+              S.cum32[j + 4] = out[4]; S.cum32[j + 5] = out[5];
+              S.cum32[j + 6] = out[6]; S.cum32[j + 7] = out[7];
             }
           }
           for (; j < jx; j++) {
@@ -336,6 +356,7 @@ __global__ void __launch_bounds__(kCtaThreads)
           }
         }
         __syncthreads();
+        if (tid == 0 && e == 0) TL_STAMP(wbase + 3);
         const int ek = S.misc[13];
         if (ek != 0x7fffffff) {
           err_code = ek & 0xff;
@@ -349,10 +370,11 @@ __global__ void __launch_bounds__(kCtaThreads)
           const StepSt stv = S.st[sidx];
           const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
           float* __restrict__ dst = P + rr;
+          // branch-free: every draw is computed, at-rest records select 0
           auto draw = [&](uint32_t k, double a, double b) -> float {
-            if (!emit) return 0.f;
             const uint2 wv = ring2[((eo + 2u * k) & kMask) >> 1];
-            return __double2float_rn(uniform_rn(a, b, rand53(wv.x, wv.y)));
+            const float v = __double2float_rn(uniform_rn(a, b, rand53(wv.x, wv.y)));
+            return emit ? v : 0.f;
           };
           RecV<float> v;
           float mq = 0.f, mqd = 0.f;

@@ -9,7 +9,6 @@
 #include "tl_label.cuh"
 #include "tl_synth.cuh"
 #include "tl_synth_cta.cuh"
-#include "tl_realize_seg.cuh"
 #include "tl_filter.cuh"
 
 namespace {
@@ -244,10 +243,7 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
   return check_launch();
 }
 
-static int fuzz_cap(const tl_fuzz_cfg& c) { return 2 + (c.max_events + 4) * c.max_gap + c.max_tail; }
-static int seg_len(int n_env, int cap) { return n_env <= 24 * sm_count() ? 64 : cap; }
-
-static int launch_synth(SynthParams& sp, bool fuzz, void* stream, SegPartial* parts = nullptr) {
+static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   const int rows_smem = 32 * kRowWords * 4;
   if (fuzz) {
     if (sp.n_env <= 32 * sm_count()) {  // latency-bound batch: one episode per warp
@@ -260,21 +256,6 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream, SegPartial* pa
   } else {
     set_max_smem(k_seed_states, rows_smem);
     k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
-  }
-  if (fuzz && parts && sp.out.dof <= 7) {
-    // segment-parallel realize + label (tl_realize_seg.cuh), then finalize
-    SegParams q;
-    q.sp = sp;
-    q.seg = seg_len(sp.n_env, sp.cap_per_env);
-    q.max_seg = (sp.cap_per_env + q.seg - 1) / q.seg;
-    q.parts = parts;
-    const int smem = kSegWarps * (int)sizeof(SegWarp);
-    set_max_smem(k_realize_seg<7>, smem);
-    const int64_t items = (int64_t)sp.n_env * q.max_seg;
-    k_realize_seg<7><<<(unsigned)((items + kSegWarps - 1) / kSegWarps), kSegWarps * 32, smem,
-                       S(stream)>>>(q);
-    k_seg_finalize<<<(sp.n_env + 127) / 128, 128, 0, S(stream)>>>(q);
-    return check_launch();
   }
   // realize + label: one 2-warp CTA per episode (tl_synth_cta.cuh)
   const bool small = sp.out.dof <= 7;
@@ -294,10 +275,8 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
   const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
-  const int cap = cfg ? fuzz_cap(*cfg) : 4096;
-  const size_t max_seg = (size_t)((cap + 63) / 64);
   return align256(n * kMtN * 4) + align256(n * sizeof(tl_script)) + align256(n * ms) +
-         align256(n * ms * 4) + align256(n * max_seg * sizeof(SegPartial));
+         align256(n * ms * 4);
 }
 
 size_t tl_realize_scratch_bytes(int32_t n_env) {
@@ -327,9 +306,6 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_
   sp.step_kind = script_kind ? script_kind : reinterpret_cast<uint8_t*>(base);
   base += align256(n * ms);
   sp.step_gap = script_gap ? script_gap : reinterpret_cast<int32_t*>(base);
-  base += align256(n * ms * 4);
-  SegPartial* parts = reinterpret_cast<SegPartial*>(base);
-  if (cap_per_env > fuzz_cap(*cfg)) parts = nullptr;  // scratch sized for the cfg capacity
   sp.seeds = seeds;
   sp.fuzz_subtask = subtask;
   sp.cfg = *cfg;
@@ -341,7 +317,7 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_
   sp.out = *out;
   sp.step_mask = step_mask;
   sp.labels = labels;
-  return launch_synth(sp, true, stream, parts);
+  return launch_synth(sp, true, stream);
 }
 
 int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t* step_gap,
