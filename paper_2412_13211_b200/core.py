@@ -128,20 +128,23 @@ def pack_trajectories(trajs, th_base: Optional[Thresholds] = None, force_f64=Fal
         if t.header.arm_dof != dof:
             raise ValueError("all trajectories of a batch must share arm_dof")
     n_rec = np.array([len(t.records) for t in trajs], np.int32)
+    # episodes start on 4-record boundaries so the label kernel can use
+    # 128-bit loads (tl_label.cuh label_vec4); the gaps are zero padding
+    n_pad = (n_rec.astype(np.int64) + 3) & ~3
     rec_start = np.zeros(len(trajs), np.int64)
     if len(trajs) > 1:
-        rec_start[1:] = np.cumsum(n_rec[:-1], dtype=np.int64)
-    R = int(n_rec.sum())
+        rec_start[1:] = np.cumsum(n_pad[:-1], dtype=np.int64)
+    R = int(n_pad.sum())
     F = 2 * dof + 9
-    planes = np.empty((F, max(R, 1)), np.float64)
-    grasped = np.zeros(max(R, 1), np.uint8)
+    planes = np.zeros((F, max(R, 4)), np.float64)
+    grasped = np.zeros(max(R, 4), np.uint8)
     table = CsetTable()
     env_cset = np.zeros(len(trajs), np.int32)
-    r = 0
     for i, t in enumerate(trajs):
         h = t.header
         recs = t.records
         n = len(recs)
+        r = int(rec_start[i])
         if n:
             for rec in recs:
                 if len(rec.q_arm) != dof or len(rec.qd_arm) != dof:
@@ -151,7 +154,6 @@ def pack_trajectories(trajs, th_base: Optional[Thresholds] = None, force_f64=Fal
             for j, f in enumerate(SCALAR_FIELDS):
                 planes[2 * dof + j, r:r + n] = [getattr(rec, f) for rec in recs]
             grasped[r:r + n] = [1 if rec.grasped else 0 for rec in recs]
-        r += n
         if len(h.rest_arm) != dof:
             raise ValueError(f"joint vector length mismatch: {dof} vs {len(h.rest_arm)}")
         env_cset[i] = table.add(SUBTASK_ORDER.index(h.subtask_kind),
@@ -290,7 +292,8 @@ def classify_lists(kinds_list, subtasks, d0s, d0_none, rules=None):
 
 def fuzz_capacity(cfg) -> int:
     """upper bound of records per fuzz episode (synth.py:363-507, :298-310)"""
-    return 2 + (cfg.max_events + 4) * cfg.max_gap + cfg.max_tail
+    n = 2 + (cfg.max_events + 4) * cfg.max_gap + cfg.max_tail
+    return (n + 3) & ~3  # 4-record aligned episode slots (128-bit label loads)
 
 
 @dataclass
@@ -374,12 +377,13 @@ def realize_batch(scripts_np, step_kind, step_gap, th_realize: Thresholds, label
         g = step_gap[s["step_off"]:s["step_off"] + s["n_steps"]]
         tmin = 0 if s["n_steps"] else 1
         n_rec[i] = max(2, 1 + int(np.sum(np.maximum(g, 0))) + max(int(s["tail"]), tmin))
+    n_pad = (n_rec + 3) & ~3  # 4-record aligned episode slots
     rec_start = np.zeros(n, np.int64)
     if n > 1:
-        rec_start[1:] = np.cumsum(n_rec[:-1])
-    R = int(n_rec.sum())
-    planes = torch.empty((2 * dof + 9, max(R, 1)), dtype=torch.float32, device=dev)
-    grasped = torch.empty(max(R, 1), dtype=torch.uint8, device=dev)
+        rec_start[1:] = np.cumsum(n_pad[:-1])
+    R = int(n_pad.sum())
+    planes = torch.zeros((2 * dof + 9, max(R, 4)), dtype=torch.float32, device=dev)
+    grasped = torch.zeros(max(R, 4), dtype=torch.uint8, device=dev)
     rb = RecordBatch(planes, grasped, torch.from_numpy(rec_start).to(dev),
                      torch.from_numpy(n_rec.astype(np.int32)).to(dev), dof)
     labels = torch.empty((max(n, 1), 24), dtype=torch.uint8, device=dev)

@@ -399,6 +399,127 @@ __device__ __forceinline__ void close_cut(const tl_cset& c, double a0, float& ru
   ru = __double2float_ru(d);
 }
 
+// ---- K1 vector path: 4 consecutive records per lane ----------------------------
+__device__ __forceinline__ float4 ldf4(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));  // streamed once: evict-first
+}
+__device__ __forceinline__ float f4get(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+
+__device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, int64_t rs, int n,
+                                        float sc_ru, double sc_d, LState& S,
+                                        uint8_t* step_mask, uint8_t* step_success) {
+  const int lane = lane_id();
+  const float* __restrict__ P = reinterpret_cast<const float*>(R.planes);
+  const int64_t stride = R.plane_stride;
+  const int dof = R.dof, f0 = 2 * dof;
+  const int sub = c.subtask;
+  for (int t0 = 0; t0 < n; t0 += 128) {
+    const int tb = t0 + 4 * lane;          // first record of this lane
+    const bool any = tb < n;
+    const int64_t r = rs + tb;
+    float4 der, cum, vx, vy, om, tor, dist, force, art, mq, mqd;
+    uint32_t g4 = 0;
+    if (any) {
+      der = ldf4(P + (f0 + 4) * stride + r);
+      cum = ldf4(P + (f0 + 7) * stride + r);
+      vx = ldf4(P + (f0 + 1) * stride + r);
+      vy = ldf4(P + (f0 + 2) * stride + r);
+      om = ldf4(P + (f0 + 3) * stride + r);
+      if (sub == TL_PICK) {
+        force = ldf4(P + (f0 + 6) * stride + r);
+        g4 = __ldcs(reinterpret_cast<const unsigned int*>(R.grasped + r));
+      } else if (sub == TL_PLACE) {
+        tor = ldf4(P + f0 * stride + r);
+        dist = ldf4(P + (f0 + 5) * stride + r);
+        g4 = __ldcs(reinterpret_cast<const unsigned int*>(R.grasped + r));
+      } else {
+        tor = ldf4(P + f0 * stride + r);
+        force = ldf4(P + (f0 + 6) * stride + r);
+        art = ldf4(P + (f0 + 8) * stride + r);
+      }
+      // Python max() of |q_i| and |qd_i| per record (predicates.py:20, :24)
+      for (int i = 0; i < dof; i++) {
+        const float4 q = ldf4(P + i * stride + r);
+        const float4 qd = ldf4(P + (dof + i) * stride + r);
+        if (i == 0) {
+          mq = make_float4(fabsf(q.x), fabsf(q.y), fabsf(q.z), fabsf(q.w));
+          mqd = make_float4(fabsf(qd.x), fabsf(qd.y), fabsf(qd.z), fabsf(qd.w));
+        } else {
+          mq = make_float4(pymax_step(mq.x, fabsf(q.x)), pymax_step(mq.y, fabsf(q.y)),
+                           pymax_step(mq.z, fabsf(q.z)), pymax_step(mq.w, fabsf(q.w)));
+          mqd = make_float4(pymax_step(mqd.x, fabsf(qd.x)), pymax_step(mqd.y, fabsf(qd.y)),
+                            pymax_step(mqd.z, fabsf(qd.z)), pymax_step(mqd.w, fabsf(qd.w)));
+        }
+      }
+    }
+    uint32_t ind[4], err[4], m[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      ind[j] = 0;
+      err[j] = 0;
+      if (tb + j < n) {
+        RecV<float> v;
+        v.der = f4get(der, j);
+        v.cum = f4get(cum, j);
+        v.vx = f4get(vx, j);
+        v.vy = f4get(vy, j);
+        v.om = f4get(om, j);
+        v.qdm = f4get(mqd, j);
+        v.jm = f4get(mq, j);
+        v.jm_d = 0.0;
+        v.tor = 0.f; v.dist = 0.f; v.force = 0.f; v.art = 0.f; v.g = false;
+        if (sub == TL_PICK) {
+          v.force = f4get(force, j);
+          v.g = (g4 >> (8 * j)) & 0xffu;
+        } else if (sub == TL_PLACE) {
+          v.tor = f4get(tor, j);
+          v.dist = f4get(dist, j);
+          v.g = (g4 >> (8 * j)) & 0xffu;
+        } else {
+          v.tor = f4get(tor, j);
+          v.force = f4get(force, j);
+          v.art = f4get(art, j);
+        }
+        record_bits(c, v, sc_ru, sc_d, ind[j], err[j]);
+        if (step_success) step_success[r + j] = (err[j] & ERR_SUCC) ? 2 : ((ind[j] & IND_SUCCESS) ? 1 : 0);
+      }
+    }
+    uint32_t prev = __shfl_up_sync(kFull, ind[3], 1);
+    if (lane == 0) prev = S.prev_ind;
+    uint32_t cnt = 0, eor = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const bool ok = tb + j < n && tb + j > 0;
+      m[j] = ok ? edge_mask(sub, j == 0 ? prev : ind[j - 1], ind[j]) : 0u;
+      cnt += __popc(m[j]);
+      eor |= (tb + j < n) ? err[j] : 0u;
+      if (step_mask && tb + j < n) step_mask[r + j] = (uint8_t)m[j];
+    }
+    const int incl = warp_incl_scan((int)cnt);
+    const int excl = incl - (int)cnt;
+#pragma unroll
+    for (int k = 0; k < 7; k++) {
+      // position (within the lane's events) of the lane's last event of kind k
+      int pos = -1, before = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if ((m[j] >> k) & 1u) pos = before + __popc(m[j] & ((1u << k) - 1u));
+        before += __popc(m[j]);
+      }
+      const unsigned bal = __ballot_sync(kFull, pos >= 0);
+      if (bal) {
+        const int L = 31 - __clz(bal);
+        S.last[k] = S.size + __shfl_sync(kFull, excl + pos, L);
+      }
+    }
+    S.size += __shfl_sync(kFull, incl, 31);
+    S.err_any |= __reduce_or_sync(kFull, eor);
+    S.prev_ind = __shfl_sync(kFull, ind[3], 31);
+  }
+}
+
 // ---- K1: label_records -------------------------------------------------------
 constexpr int kLabelWarps = 8;
 
@@ -413,6 +534,8 @@ __global__ void __launch_bounds__(kLabelWarps * 32)
   const T* __restrict__ P = reinterpret_cast<const T*>(R.planes);
   const int64_t stride = R.plane_stride;
   const int dof = R.dof;
+  const bool vec_ok = (stride & 3) == 0 && (reinterpret_cast<uintptr_t>(R.planes) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(R.grasped) & 3) == 0;
   for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
     stage_cset(&s_cs[warp], &csets[env_cset[e]]);
     const tl_cset& c = s_cs[warp];
@@ -440,6 +563,13 @@ __global__ void __launch_bounds__(kLabelWarps * 32)
     double sc_d = 0.0;
     if (c.subtask == TL_PLACE) d0 = (double)P[(f0 + 5) * stride + rs];
     if (c.subtask == TL_CLOSE && n > 0) close_cut(c, (double)P[(f0 + 8) * stride + rs], sc_ru, sc_d);
+    // f32 episodes whose records are 16-byte aligned: 4 records per lane,
+    // 128-bit loads (k_label_vec4); otherwise one record per lane below.
+    if (sizeof(T) == 4 && c.rest_zero && (rs & 3) == 0 && vec_ok) {
+      label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
+      if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
+      continue;
+    }
     for (int t0 = 0; t0 < n; t0 += 32) {
       const int t = t0 + lane;
       const bool valid = t < n;

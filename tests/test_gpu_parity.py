@@ -26,15 +26,31 @@ def TH():
     return Thresholds
 
 
-def corpus_batch(C, TH, c: Corpus, dtype=np.float32, overrides=None):
-    """fixture corpus -> RecordBatch + csets (planes copied verbatim)."""
+def corpus_batch(C, TH, c: Corpus, dtype=np.float32, overrides=None, align=False):
+    """fixture corpus -> RecordBatch + csets.  align=False copies the planes
+    verbatim (packed episodes: the one-record-per-lane label path); align=True
+    re-packs every episode at a 4-record boundary (the 128-bit label path)."""
     dev = torch.device("cuda")
-    planes = torch.from_numpy(np.ascontiguousarray(c.planes.astype(dtype))).to(dev)
-    if planes.shape[1] == 0:
-        planes = torch.zeros((planes.shape[0], 1), dtype=planes.dtype, device=dev)
-    g = torch.from_numpy(np.ascontiguousarray(c.grasped) if len(c.grasped) else np.zeros(1, np.uint8)).to(dev)
-    rs = torch.from_numpy(c.rec_off[:-1].copy()).to(dev)
-    nr = torch.from_numpy(np.diff(c.rec_off).astype(np.int32)).to(dev)
+    nrec = np.diff(c.rec_off).astype(np.int64)
+    if align:
+        slot = (nrec + 3) & ~3
+        starts = np.concatenate([[0], np.cumsum(slot)[:-1]]).astype(np.int64)
+        hp = np.full((c.planes.shape[0], max(int(slot.sum()), 4)), np.nan, dtype)
+        hg = np.zeros(hp.shape[1], np.uint8)
+        for i in range(c.n):
+            a, b = c.rec_off[i], c.rec_off[i + 1]
+            hp[:, starts[i]:starts[i] + b - a] = c.planes[:, a:b]
+            hg[starts[i]:starts[i] + b - a] = c.grasped[a:b]
+        planes = torch.from_numpy(hp).to(dev)
+        g = torch.from_numpy(hg).to(dev)
+        rs = torch.from_numpy(starts).to(dev)
+    else:
+        planes = torch.from_numpy(np.ascontiguousarray(c.planes.astype(dtype))).to(dev)
+        if planes.shape[1] == 0:
+            planes = torch.zeros((planes.shape[0], 1), dtype=planes.dtype, device=dev)
+        g = torch.from_numpy(np.ascontiguousarray(c.grasped) if len(c.grasped) else np.zeros(1, np.uint8)).to(dev)
+        rs = torch.from_numpy(c.rec_off[:-1].copy()).to(dev)
+    nr = torch.from_numpy(nrec.astype(np.int32)).to(dev)
     rb = C.RecordBatch(planes, g, rs, nr, DOF)
     tab = C.CsetTable()
     env = np.zeros(c.n, np.int32)
@@ -71,33 +87,64 @@ def check_labels(res, c: Corpus, err_type=None):
         assert lab["n_events"][i] == len(want_k)
 
 
+@pytest.mark.parametrize("align", [False, True])
 @pytest.mark.parametrize("kind", range(4))
-def test_label_fuzz_fixtures(C, TH, kind):
+def test_label_fuzz_fixtures(C, TH, kind, align):
     c = fuzz_corpus(kind)
-    rb, env, cs, n = corpus_batch(C, TH, c)
+    rb, env, cs, n = corpus_batch(C, TH, c, align=align)
     res = C.label_records(rb, env, cs, n)
     check_labels(res, c)
 
 
-def test_label_defining_and_long(C, TH):
+@pytest.mark.parametrize("align", [False, True])
+def test_label_defining_and_long(C, TH, align):
     for c in (Corpus(npz("defining")), Corpus(npz("long"))):
-        rb, env, cs, n = corpus_batch(C, TH, c)
+        rb, env, cs, n = corpus_batch(C, TH, c, align=align)
         check_labels(C.label_records(rb, env, cs, n), c)
 
 
+@pytest.mark.parametrize("align", [False, True])
 @pytest.mark.parametrize("tag,dtype", [("f32_", np.float32), ("f64_", np.float64)])
-def test_label_crafted(C, TH, tag, dtype):
+def test_label_crafted(C, TH, tag, dtype, align):
     d = npz("crafted")
     c = Corpus(d, tag)
     fields = list(d["threshold_fields"])
     ov = [dict(zip(fields, map(float, d[tag + "override"][i]))) if d[tag + "has_override"][i] else None
           for i in range(c.n)]
-    rb, env, cs, n = corpus_batch(C, TH, c, dtype, ov)
+    rb, env, cs, n = corpus_batch(C, TH, c, dtype, ov, align=align)
     res = C.label_records(rb, env, cs, n, want_success=True)
     check_labels(res, c, d[tag + "err_type"])
     # per-record success_step (predicates.py:75-94), incl. raising records
-    got = res.step_success.cpu().numpy()[:c.rec_off[-1]]
-    assert np.array_equal(got, d[tag + "success_step"])
+    got = res.step_success.cpu().numpy()
+    if align:
+        rs = rb.rec_start.cpu().numpy()
+        got = np.concatenate([got[rs[i]:rs[i] + c.rec_off[i + 1] - c.rec_off[i]] for i in range(c.n)])
+    assert np.array_equal(got[:c.rec_off[-1]], d[tag + "success_step"])
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_label_kernel_matches_fused_synth_labels(C, TH, kind):
+    """tl_label_records over fuzz output (4-record aligned slots, 128-bit
+    path) == the labels and step masks tl_fuzz folded while generating."""
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_gap=64, max_tail=64)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 4000
+    sb = C.fuzz_batch(np.arange(n) + 31337, kind, cfg, TH(), cs, want_scripts=True)
+    from paper_2412_13211_b200 import _lib as L
+    art = sb.scripts.cpu().numpy().reshape(-1).view(L.SCRIPT_DTYPE)["art_kind"]
+    env = torch.from_numpy((3 * kind + art).astype(np.int32)).to("cuda")
+    lab_kind = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    res = C.label_records(sb.records, env, cs, 12, want_events=False)
+    a = sb.labels.cpu().numpy()
+    b = res.labels.cpu().numpy()
+    assert np.all(lab_kind["status"] == 0)
+    assert np.array_equal(a, b)
+    rs = sb.records.rec_start.cpu().numpy()
+    nr = sb.records.n_rec.cpu().numpy()
+    ma, mb = sb.step_mask.cpu().numpy(), res.step_mask.cpu().numpy()
+    for e in range(0, n, 7):
+        assert np.array_equal(ma[rs[e]:rs[e] + nr[e]], mb[rs[e]:rs[e] + nr[e]]), e
 
 
 def _fuzz_records(sb, e):
@@ -173,9 +220,11 @@ def test_realize_defining_and_long(C, TH):
         sb = C.realize_batch(arr, k, g, TH(), cs)
         lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
         planes = sb.records.planes.cpu().numpy()
+        rs = sb.records.rec_start.cpu().numpy()
         for i in range(c.n):
             a, b = c.rec_off[i], c.rec_off[i + 1]
-            assert same_bits_f32(planes[:, a:b], c.planes[:, a:b]), i
+            assert rs[i] % 4 == 0
+            assert same_bits_f32(planes[:, rs[i]:rs[i] + b - a], c.planes[:, a:b]), i
             assert lab["status"][i] == 0 and lab["mode"][i] == c.mode[i], i
 
 
