@@ -50,6 +50,12 @@ enum {
   TL_EV_OPEN, TL_EV_SUCCESS, TL_EV_EXCESSIVE_COLLISIONS
 };
 /* EventScript.initial_art_level strings (synth.py:71) */
+/* batched env actions (tl_env_step): 0..13 = EventKind applied at this
+ * step, or one of these */
+enum { TL_ACT_HOLD = 255,     /* no event: _advance_cum + _emit (synth.py:198-201) */
+       TL_ACT_IDLE = 254,     /* env does not advance: no record, mask 0 */
+       TL_ACT_BAD_GAP = 253   /* raise InfeasibleScript "event gap must be >= 1" */
+};
 enum { TL_LVL_LOW = 0, TL_LVL_SLIGHT = 1, TL_LVL_OPEN = 2, TL_LVL_HIGH = 3,
        TL_LVL_CLOSED = 4 };
 
@@ -256,6 +262,53 @@ int tl_realize(const tl_script* scripts, const uint8_t* step_kind,
                const tl_rules* rules /* host */, tl_records* out,
                uint8_t* step_mask, tl_label* labels, void* scratch,
                void* stream);
+
+/* ---- K3 as an environment: reset / step(actions) -------------------------
+ * synth.py:100-302 split at the record boundary: reset = _Realizer.__init__
+ * + the t = 0 _emit; each step = _advance_cum, _apply(action) unless
+ * TL_ACT_HOLD, _emit; one record per env per step.  The edge events of each
+ * new record are folded online (events.py:94-193), so tl_env_labels
+ * classifies the episode so far without re-reading records.
+ * state: opaque device buffer of tl_env_state_bytes(n_env) bytes (realize
+ * thresholds, label csets, 128 B per env + the env's MT19937 state).
+ * Observations are time-major f32 planes (the tl_records plane order):
+ *   obs[f*obs_stride + k*n_env + e], obs_grasped[k*n_env + e],
+ *   step_mask[k*n_env + e] (EVENT_ORDER bits of the events that record fired)
+ * for step k of the call (reset: k = 0).  An infeasible action (InfeasibleScript
+ * in the reference) stops that env: status/err in its label, nothing written.
+ * realize(script, seed) == tl_env_reset(script with .seed) followed by the
+ * tl_env_script_actions stream; fuzz(seed) == tl_env_reset_fuzz + the same. */
+size_t tl_env_state_bytes(int32_t n_env);
+int tl_env_reset(void* state, int32_t n_env, int32_t dof, const tl_script* scripts,
+                 const tl_thresholds* th_realize /* host */,
+                 const tl_cset* label_csets /* device [4 subtasks][3 art] */,
+                 float* obs, int64_t obs_stride, uint8_t* obs_grasped,
+                 uint8_t* step_mask, void* stream);
+/* random_script(seed, subtask, cfg) initial conditions + realize RNG seeded
+ * with seed ^ 0x5EED (synth.py:510-515); the sampled scripts go to
+ * scripts / script_kind / script_gap (steps at e*(cfg.max_events+4)) so
+ * tl_env_script_actions replays fuzz(seed). */
+int tl_env_reset_fuzz(void* state, const int64_t* seeds, int32_t n_env, int32_t subtask,
+                      const tl_fuzz_cfg* cfg /* host */,
+                      const tl_thresholds* th_realize /* host */,
+                      const tl_cset* label_csets, tl_script* scripts,
+                      uint8_t* script_kind, int32_t* script_gap, float* obs,
+                      int64_t obs_stride, uint8_t* obs_grasped, uint8_t* step_mask,
+                      void* stream);
+int tl_env_step(void* state, int32_t n_env, int32_t dof,
+                const uint8_t* actions /* [k_steps][n_env] */, int32_t k_steps,
+                float* obs, int64_t obs_stride, uint8_t* obs_grasped,
+                uint8_t* step_mask, void* stream);
+/* label of every env's episode so far; infeasible envs report the InfeasibleScript
+ * code with err_index = record index of the raising action and pad = that action.
+ * n_rec (optional) = records emitted (0 for failed envs). */
+int tl_env_labels(const void* state, int32_t n_env, const tl_rules* rules /* host */,
+                  tl_label* labels, int32_t* n_rec, void* stream);
+/* scripts -> actions[k][e] for records t = t0 + k (TL_ACT_HOLD between events,
+ * TL_ACT_IDLE past the script's record count). */
+int tl_env_script_actions(const tl_script* scripts, const uint8_t* step_kind,
+                          const int32_t* step_gap, int32_t n_env, int32_t t0,
+                          int32_t k_steps, uint8_t* actions, void* stream);
 
 /* K5: filter_labels selection (pipeline.py:276-338).  Labels are already
  * in episode_id order.  bucket[i] in [-1, n_buckets): the (quota key,

@@ -39,6 +39,7 @@ ERR_D0_NONE_GT = 9
 INF_FIRST, INF_LAST = 20, 41
 ERR_SCRIPT_CAPACITY = 50
 E_INVALID, E_CUDA, E_CAPACITY = 100, 101, 102
+ACT_HOLD, ACT_IDLE, ACT_BAD_GAP = 255, 254, 253
 
 
 class NativeUnavailable(RuntimeError):
@@ -158,6 +159,14 @@ def lib():
         "tl_compact_records": ([P(Records_c), i32, vp, P(Records_c), vp], ctypes.c_int),
         "tl_eval_predicates": ([P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp],
                                ctypes.c_int),
+        "tl_env_state_bytes": ([i32], ctypes.c_size_t),
+        "tl_env_reset": ([vp, i32, i32, vp, P(Thresholds_c), vp, vp, i64, vp, vp, vp],
+                         ctypes.c_int),
+        "tl_env_reset_fuzz": ([vp, vp, i32, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
+                               vp, vp, vp, i64, vp, vp, vp], ctypes.c_int),
+        "tl_env_step": ([vp, i32, i32, vp, i32, vp, i64, vp, vp, vp], ctypes.c_int),
+        "tl_env_labels": ([vp, i32, vp, vp, vp, vp], ctypes.c_int),
+        "tl_env_script_actions": ([vp, vp, vp, i32, i32, i32, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -176,7 +185,8 @@ def exported_symbols():
             "tl_realize", "tl_filter_scratch_bytes", "tl_filter_select",
             "tl_mode_histogram", "tl_eval_predicates", "tl_scan_counts",
             "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes",
-            "tl_scan_emit_events"]
+            "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
+            "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions"]
 
 
 def check(rc, what):

@@ -30,6 +30,11 @@ def thresholds_c(th: Thresholds) -> L.Thresholds_c:
     return L.Thresholds_c(*[float(getattr(th, f)) for f in THRESHOLD_FIELDS])
 
 
+def fuzz_cfg_c(cfg) -> L.FuzzCfg_c:
+    return L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0,
+                       float(cfg.edge_density), float(cfg.success_prob))
+
+
 def cset_build(subtask: int, art_kind: int, qmin: float, qmax: float, dof: int,
                rest_arm, rest_tor: float, th: Thresholds) -> bytes:
     """tl_cset_build (host function of the library) -> raw struct bytes."""

@@ -353,10 +353,9 @@ __device__ __forceinline__ int label_status(const tl_cset& c, uint32_t err_any) 
   return TL_OK;
 }
 
-// Finalise an episode: status + classify; writes the label (lane 0 only).
-__device__ __forceinline__ void finish_label(const tl_cset& c, const LState& S,
-                                             double d0, const tl_rules& rules,
-                                             tl_label* out) {
+// Finalise an episode: status + classify.
+__device__ __forceinline__ tl_label make_label(const tl_cset& c, const LState& S, double d0,
+                                               const tl_rules& rules) {
   tl_label L;
   L.status = label_status(c, S.err_any);
   L.n_events = 0;
@@ -381,6 +380,14 @@ __device__ __forceinline__ void finish_label(const tl_cset& c, const LState& S,
       L.flags = fl;
     }
   }
+  return L;
+}
+
+// warp-uniform state: lane 0 writes the label
+__device__ __forceinline__ void finish_label(const tl_cset& c, const LState& S,
+                                             double d0, const tl_rules& rules,
+                                             tl_label* out) {
+  const tl_label L = make_label(c, S, d0, rules);
   if (lane_id() == 0) *out = L;
 }
 

@@ -10,6 +10,7 @@
 #include "tl_synth.cuh"
 #include "tl_synth_cta.cuh"
 #include "tl_filter.cuh"
+#include "tl_env.cuh"
 
 namespace {
 
@@ -342,6 +343,165 @@ int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t
   sp.step_mask = step_mask;
   sp.labels = labels;
   return launch_synth(sp, false, stream);
+}
+
+// ---- batched env ------------------------------------------------------------
+size_t tl_env_state_bytes(int32_t n_env) { return env_bytes(n_env > 0 ? n_env : 1); }
+
+static EnvParams env_params(void* state, int32_t n_env, int32_t dof) {
+  EnvParams ep;
+  memset(&ep, 0, sizeof(ep));
+  char* b = reinterpret_cast<char*>(state);
+  ep.hdr = reinterpret_cast<EnvHdr*>(b);
+  ep.st = reinterpret_cast<EnvSt*>(b + env_st_off());
+  ep.mt = reinterpret_cast<uint32_t*>(b + env_mt_off(n_env));
+  ep.n_env = n_env;
+  ep.dof = dof;
+  return ep;
+}
+
+static int env_write_hdr(const EnvParams& ep, const tl_thresholds* th, const tl_cset* csets,
+                         int32_t n_env, int32_t dof, void* stream) {
+  // pageable source: cudaMemcpyAsync stages it before returning
+  EnvHdr h;
+  memset(&h, 0, sizeof(h));
+  h.th = *th;
+  h.n_env = n_env;
+  h.dof = dof;
+  if (cudaMemcpyAsync(&ep.hdr->th, &h.th, sizeof(h.th), cudaMemcpyHostToDevice, S(stream)) ||
+      cudaMemcpyAsync(&ep.hdr->n_env, &h.n_env, 16, cudaMemcpyHostToDevice, S(stream)) ||
+      cudaMemcpyAsync(ep.hdr->cs, csets, sizeof(h.cs), cudaMemcpyDeviceToDevice, S(stream)))
+    return TL_E_CUDA;
+  return TL_OK;
+}
+
+static int env_launch_reset(EnvParams& ep, void* stream) {
+  const int grid = (ep.n_env + kEnvThreads - 1) / kEnvThreads;
+  if (ep.dof <= 7) {
+    set_max_smem(k_env_reset<7>, (int)sizeof(EnvSmem<7>));
+    k_env_reset<7><<<grid, kEnvThreads, sizeof(EnvSmem<7>), S(stream)>>>(ep);
+  } else {
+    set_max_smem(k_env_reset<16>, (int)sizeof(EnvSmem<16>));
+    k_env_reset<16><<<grid, kEnvThreads, sizeof(EnvSmem<16>), S(stream)>>>(ep);
+  }
+  return check_launch();
+}
+
+static bool env_obs_ok(const float* obs, int64_t stride, int64_t cols) {
+  return obs && stride >= cols;
+}
+
+int tl_env_reset(void* state, int32_t n_env, int32_t dof, const tl_script* scripts,
+                 const tl_thresholds* th_realize, const tl_cset* label_csets, float* obs,
+                 int64_t obs_stride, uint8_t* obs_grasped, uint8_t* step_mask, void* stream) {
+  if (!state || !scripts || !th_realize || !label_csets || n_env < 0 || dof < 1 ||
+      dof > TL_MAX_DOF || (n_env > 0 && !env_obs_ok(obs, obs_stride, n_env)))
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  EnvParams ep = env_params(state, n_env, dof);
+  if (int rc = env_write_hdr(ep, th_realize, label_csets, n_env, dof, stream)) return rc;
+  SynthParams sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.scripts = const_cast<tl_script*>(scripts);
+  sp.states = ep.mt;
+  sp.n_env = n_env;
+  const int rows_smem = 32 * kRowWords * 4;
+  set_max_smem(k_seed_states, rows_smem);
+  k_seed_states<<<(n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
+  ep.scripts = scripts;
+  ep.obs = obs;
+  ep.obs_stride = obs_stride;
+  ep.obs_grasped = obs_grasped;
+  ep.step_mask = step_mask;
+  return env_launch_reset(ep, stream);
+}
+
+int tl_env_reset_fuzz(void* state, const int64_t* seeds, int32_t n_env, int32_t subtask,
+                      const tl_fuzz_cfg* cfg, const tl_thresholds* th_realize,
+                      const tl_cset* label_csets, tl_script* scripts, uint8_t* script_kind,
+                      int32_t* script_gap, float* obs, int64_t obs_stride, uint8_t* obs_grasped,
+                      uint8_t* step_mask, void* stream) {
+  if (!state || !seeds || !cfg || !th_realize || !label_csets || !scripts || !script_kind ||
+      !script_gap || n_env < 0 || subtask < 0 || subtask > 3 || cfg->max_gap < 1 ||
+      cfg->max_tail < 1 || cfg->max_events < 0 || cfg->max_events + 4 > kMaxSteps ||
+      (n_env > 0 && !env_obs_ok(obs, obs_stride, n_env)))
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  const int dof = 7;  // random_script builds arm_dof = 7 scripts (synth.py:63-74)
+  EnvParams ep = env_params(state, n_env, dof);
+  if (int rc = env_write_hdr(ep, th_realize, label_csets, n_env, dof, stream)) return rc;
+  SynthParams sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.seeds = seeds;
+  sp.fuzz_subtask = subtask;
+  sp.cfg = *cfg;
+  sp.scripts = scripts;
+  sp.step_kind = script_kind;
+  sp.step_gap = script_gap;
+  sp.states = ep.mt;
+  sp.n_env = n_env;
+  sp.cap_per_env = 0x7fffffff;
+  const int rows_smem = 32 * kRowWords * 4;
+  if (n_env <= 32 * sm_count()) {
+    k_fuzz_reset<1><<<n_env, 32, 2 * kRowWords * 4, S(stream)>>>(sp);
+  } else {
+    set_max_smem(k_fuzz_reset<16>, rows_smem);
+    k_fuzz_reset<16><<<(n_env + 15) / 16, 32, rows_smem, S(stream)>>>(sp);
+  }
+  ep.scripts = scripts;
+  ep.obs = obs;
+  ep.obs_stride = obs_stride;
+  ep.obs_grasped = obs_grasped;
+  ep.step_mask = step_mask;
+  return env_launch_reset(ep, stream);
+}
+
+int tl_env_step(void* state, int32_t n_env, int32_t dof, const uint8_t* actions,
+                int32_t k_steps, float* obs, int64_t obs_stride, uint8_t* obs_grasped,
+                uint8_t* step_mask, void* stream) {
+  if (!state || n_env < 0 || dof < 1 || dof > TL_MAX_DOF || k_steps < 0 ||
+      (n_env > 0 && k_steps > 0 && (!actions || !env_obs_ok(obs, obs_stride, (int64_t)k_steps * n_env))))
+    return TL_E_INVALID;
+  if (n_env == 0 || k_steps == 0) return TL_OK;
+  EnvParams ep = env_params(state, n_env, dof);
+  ep.actions = actions;
+  ep.k_steps = k_steps;
+  ep.obs = obs;
+  ep.obs_stride = obs_stride;
+  ep.obs_grasped = obs_grasped;
+  ep.step_mask = step_mask;
+  const int grid = (n_env + kEnvThreads - 1) / kEnvThreads;
+  if (dof <= 7) {
+    set_max_smem(k_env_step<7>, (int)sizeof(EnvSmem<7>));
+    k_env_step<7><<<grid, kEnvThreads, sizeof(EnvSmem<7>), S(stream)>>>(ep);
+  } else {
+    set_max_smem(k_env_step<16>, (int)sizeof(EnvSmem<16>));
+    k_env_step<16><<<grid, kEnvThreads, sizeof(EnvSmem<16>), S(stream)>>>(ep);
+  }
+  return check_launch();
+}
+
+int tl_env_labels(const void* state, int32_t n_env, const tl_rules* rules, tl_label* labels,
+                  int32_t* n_rec, void* stream) {
+  if (!state || !labels || n_env < 0) return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  EnvParams ep = env_params(const_cast<void*>(state), n_env, 7);
+  ep.rules = rules_or_default(rules);
+  ep.labels = labels;
+  ep.n_rec = n_rec;
+  k_env_labels<<<(n_env + 127) / 128, 128, 0, S(stream)>>>(ep);
+  return check_launch();
+}
+
+int tl_env_script_actions(const tl_script* scripts, const uint8_t* step_kind,
+                          const int32_t* step_gap, int32_t n_env, int32_t t0, int32_t k_steps,
+                          uint8_t* actions, void* stream) {
+  if (!scripts || !step_kind || !step_gap || !actions || n_env < 0 || k_steps < 0 || t0 < 0)
+    return TL_E_INVALID;
+  if (n_env == 0 || k_steps == 0) return TL_OK;
+  k_env_script_actions<<<(n_env + 127) / 128, 128, 0, S(stream)>>>(scripts, step_kind, step_gap,
+                                                                  n_env, t0, k_steps, actions);
+  return check_launch();
 }
 
 size_t tl_filter_scratch_bytes(int64_t n, int32_t n_buckets, int32_t n_pools) {
