@@ -229,6 +229,61 @@ def label_sizing_run(L, core, lib, dev, stream, flush, n_env=1 << 19, reps=5):
             "note": "81 B/env-step read (Pick fields) + 1 B step mask + 24 B/episode label"}
 
 
+def env_api_run(dev, stream, n_env=4096, T=200, reps=10):
+    """North-star env API: BatchedSubtaskEnv.reset(fuzz seeds,
+    Place) + T scripted random-action steps per env, (a) one tl_env_step
+    launch for all T steps, (b) T single-step launches (CUDA graph).
+    Inputs resident; records + step masks written to HBM (93 + 1 B/env-step)."""
+    import torch
+    import paper_2412_13211_b200 as P
+    kind = P.SubtaskKind.Place
+    cfg = P.FuzzConfig(max_gap=64, max_tail=64)
+    env = P.BatchedSubtaskEnv(n_env)
+    seeds = torch.arange(n_env, dtype=torch.int64, device=dev) + 10_000_000
+    buf0 = env._outputs(1, None)
+    bufT = env._outputs(T, None)
+    buf1 = [env._outputs(1, None) for _ in range(T)]
+    env.reset(seeds=seeds, subtask=kind, config=cfg, out=buf0)
+    acts = env.scripted_actions(1, T)
+    records = int((acts != P.env.IDLE).sum()) + n_env
+
+    def block():
+        env.reset(seeds=seeds, subtask=kind, config=cfg, out=buf0)
+        env.step(acts, out=bufT)
+
+    def single():
+        env.reset(seeds=seeds, subtask=kind, config=cfg, out=buf0)
+        for k in range(T):
+            env.step(acts[k:k + 1], out=buf1[k])
+
+    res = {"api": "BatchedSubtaskEnv.reset(seeds, Place) + step(actions[K, N])",
+           "kernels": "k_fuzz_reset + k_env_reset + k_env_step", "n_env": n_env,
+           "steps": T, "env_steps": records}
+    hbm, _ = peaks()
+    for name, fn in (("one_launch", block), ("per_step_launch", single)):
+        for _ in range(3):
+            fn()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / reps / 1e3
+        res[name] = {"ms": 1e3 * t, "env_steps_per_s": records / t,
+                     "achieved_GBps": records * 94.0 / t / 1e9, "frac_hbm": records * 94.0 / t / 1e9 / hbm}
+    lab, nrec = env.labels()
+    assert (lab["status"] == 0).all() and int(nrec.sum()) == records
+    res["note"] = ("records = env steps actually emitted (scripts end before T -> IDLE); "
+                   "94 B/env-step written (93 B record + 1 B event mask)")
+    return res
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -406,6 +461,7 @@ def main():
         t_e2r, e2r_recs, _, d2h_rb = e2e_loop(True)
         # ---- sizing run: k_label over 2^19 x 200-step episodes
         sizing = label_sizing_run(L, core, lib, dev, stream, flush)
+        env_api = env_api_run(dev, stream)
     clk = clocks.summary()
 
     recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
@@ -467,6 +523,7 @@ def main():
                                  "note": "same, plus tl_compact_records + D2H of every "
                                          "generated record (93 B/env-step)"}},
         "label_sizing": sizing,
+        "env_api": env_api,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
                          "sample": cb_sample, "trajectories_per_sec": cb_eps},
         "clocks": clk,
