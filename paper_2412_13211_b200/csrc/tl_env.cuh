@@ -350,43 +350,98 @@ __global__ void __launch_bounds__(kEnvThreads) k_env_reset(EnvParams p) {
 }
 
 // step: k_steps records per env (actions[k][e]): _advance_cum, _apply, _emit.
+// Four lanes (a quad) share one env: the plan is computed redundantly by
+// the quad, the MT window copies, the draws and the plane stores are split
+// four ways (draw d -> lane d % 4: the pre-draws of cum / dist are draws 0..pre-1,
+// plane k is draw pre + k), and lane 0 gathers the record for the label fold.
+constexpr int kQuad = 4;
+constexpr int kEnvQThreads = 128;             // 32 envs per block
+constexpr int kEnvQPerBlock = kEnvQThreads / kQuad;
+
 template <int DOFMAX>
-__global__ void __launch_bounds__(kEnvThreads) k_env_step(EnvParams p) {
+struct EnvQSmem {
+  static constexpr int kWords = 2 * (2 + 2 * DOFMAX + 5);  // max words per step
+  static constexpr int kBuf = 2 * kWords + 1;              // old[kWords+1] + src[kWords]
+  static constexpr int kStride = 2 * kBuf + 1;             // two buffers per env; odd
+  tl_cset cs[12];
+  uint32_t buf[kEnvQPerBlock * kStride];
+};
+
+// lane q of the quad copies words j = q, q+4, ... of the window
+template <int MAXW>
+__device__ __forceinline__ void env_stage_async_q(const uint32_t* __restrict__ mt, int idx,
+                                                  uint32_t* so, uint32_t* ss, int q) {
+#pragma unroll
+  for (int j0 = 0; j0 <= MAXW; j0 += kQuad) {
+    const int j = j0 + q;
+    if (j <= MAXW) {
+      int i = idx + j;
+      i = i >= kMtN ? i - kMtN : i;
+      cp_async4(so + j, mt + i);
+    }
+  }
+#pragma unroll
+  for (int j0 = 0; j0 < MAXW; j0 += kQuad) {
+    const int j = j0 + q;
+    if (j < MAXW) {
+      int i = idx + j + kMtM;
+      i = i >= kMtN ? i - kMtN : i;
+      i = i >= kMtN ? i - kMtN : i;
+      cp_async4(ss + j, mt + i);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int DOFMAX>
+__global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
+  using SM = EnvQSmem<DOFMAX>;
   extern __shared__ __align__(16) unsigned char env_smem_raw[];
-  EnvSmem<DOFMAX>& sm = *reinterpret_cast<EnvSmem<DOFMAX>*>(env_smem_raw);
-  env_stage_csets(sm, p.hdr);
-  const int e = blockIdx.x * kEnvThreads + threadIdx.x;
-  if (e >= p.n_env) return;
+  SM& sm = *reinterpret_cast<SM*>(env_smem_raw);
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(p.hdr->cs);
+    uint32_t* d = reinterpret_cast<uint32_t*>(sm.cs);
+    for (int i = threadIdx.x; i < (int)(sizeof(sm.cs) / 4); i += blockDim.x) d[i] = __ldg(src + i);
+    __syncthreads();
+  }
+  const int q = threadIdx.x & (kQuad - 1);
+  const int le = threadIdx.x / kQuad;
+  const int e = blockIdx.x * kEnvQPerBlock + le;
+  const int qbase = lane_id() & ~(kQuad - 1);
+  const unsigned qmask = 0xFu << qbase;
+  if (e >= p.n_env) return;  // whole quads leave together
   EnvSt s;
   env_load(s, &p.st[e]);
   const int n = p.n_env;
   if (s.status || !s.active) {
     if (p.step_mask)
-      for (int k = 0; k < p.k_steps; k++) p.step_mask[(int64_t)k * n + e] = 0;
+      for (int k = q; k < p.k_steps; k += kQuad) p.step_mask[(int64_t)k * n + e] = 0;
     return;
   }
   RzConst z;
   env_rz(z, s, p.hdr->th, p.dof);
   const tl_cset& c = sm.cs[s.subtask * 3 + s.art_kind];
   uint32_t* mt = p.mt + (size_t)e * kMtN;
-  using SM = EnvSmem<DOFMAX>;
-  uint32_t* row = sm.buf + threadIdx.x * SM::kStride;
+  uint32_t* row = sm.buf + le * SM::kStride;
+  const int dof = z.dof, ne = z.ne;
+  const int64_t st = p.obs_stride;
+  const float fnan = __int_as_float(0x7fc00000);
   int cur = 0;  // buffer holding the window at s.mt_idx
-  env_stage_async<SM::kWords>(mt, s.mt_idx, row, row + SM::kWords + 1);
+  env_stage_async_q<SM::kWords>(mt, s.mt_idx, row, row + SM::kWords + 1, q);
   int a_next = p.actions[e];
   for (int k = 0; k < p.k_steps; k++) {
     const int64_t col = (int64_t)k * n + e;
     const int a = a_next;
     if (k + 1 < p.k_steps) a_next = p.actions[col + n];  // prefetch
     if (a == TL_ACT_IDLE || s.status) {
-      if (p.step_mask) p.step_mask[col] = 0;
+      if (q == 0 && p.step_mask) p.step_mask[col] = 0;
       continue;
     }
     if (a == TL_ACT_BAD_GAP) {  // run(): "event gap must be >= 1" (synth.py:301-302)
       s.status = TL_INF_GAP;
       s.err_t = s.t + 1;
       s.err_act = (uint8_t)a;
-      if (p.step_mask) p.step_mask[col] = 0;
+      if (q == 0 && p.step_mask) p.step_mask[col] = 0;
       continue;
     }
     // draw plan: known before any draw (synth.py:192-196, :205-296)
@@ -416,7 +471,7 @@ __global__ void __launch_bounds__(kEnvThreads) k_env_step(EnvParams p) {
         s.status = code;
         s.err_t = s.t + 1;
         s.err_act = (uint8_t)a;
-        if (p.step_mask) p.step_mask[col] = 0;
+        if (q == 0 && p.step_mask) p.step_mask[col] = 0;
         continue;
       }
       s.force = ps.force;
@@ -425,39 +480,106 @@ __global__ void __launch_bounds__(kEnvThreads) k_env_step(EnvParams p) {
       s.at_rest = (uint8_t)ps.at_rest;
       s.level = (uint8_t)ps.level;
     }
-    const int nw = 2 * (adv + app + (s.at_rest ? 0 : z.ne));
+    const bool emit = !s.at_rest;
+    const int pre = adv + app;
+    const int nw = 2 * (pre + (emit ? ne : 0));
     const int idx = s.mt_idx;
     const int ni = idx + nw;
     s.mt_idx = ni >= kMtN ? ni - kMtN : ni;
-    uint32_t* so = row + cur * SM::kBuf;
-    uint32_t* ss = so + SM::kWords + 1;
-    {  // next step's window into the other buffer, then wait for this one
+    const uint32_t* so = row + cur * SM::kBuf;
+    const uint32_t* ss = so + SM::kWords + 1;
+    {  // next step's window into the other buffer; this one complete quad-wide
       uint32_t* no = row + (cur ^ 1) * SM::kBuf;
-      env_stage_async<SM::kWords>(mt, s.mt_idx, no, no + SM::kWords + 1);
+      env_stage_async_q<SM::kWords>(mt, s.mt_idx, no, no + SM::kWords + 1, q);
       cp_async_wait<1>();
+      __syncwarp(qmask);
       cur ^= 1;
     }
-    int j = 0;
+    // this lane's draws: d = q, q + 4, ... over pre-draws then planes
+    double r_pre = 0.0;
+    float mq = 0.f, mqd = 0.f, sc5[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    double md = 0.0;
+    const int nd = pre + ne;
+    for (int d = q; d < nd; d += kQuad) {
+      const bool draw = d < pre || emit;
+      const double r = draw ? env_rand(mt, idx, 2 * d, so, ss) : 0.0;
+      if (d < pre) {
+        r_pre = r;  // lane 0: cum (or dist), lane 1: dist
+        continue;
+      }
+      const int kf = d - pre;  // plane
+      double lo, hi;
+      if (kf < dof) { lo = -0.3; hi = 0.3; }
+      else if (kf < 2 * dof) { lo = -0.4; hi = 0.4; }
+      else {
+        const int j = kf - 2 * dof;
+        lo = j == 0 ? -0.05 : j == 3 ? -0.3 : j == 4 ? 0.2 : -0.2;
+        hi = j == 0 ? 0.05 : j == 3 ? 0.3 : j == 4 ? 1.0 : 0.2;
+      }
+      const float v = emit ? __double2float_rn(uniform_rn(lo, hi, r)) : 0.f;
+      p.obs[(int64_t)kf * st + col] = v;
+      if (kf < dof) {
+        mq = fmaxf(mq, fabsf(v));  // generated values are never NaN: max is order-free
+        if (!c.rest_zero) md = fmax(md, fabs(__dsub_rn((double)v, c.rest_arm[kf])));
+      } else if (kf < 2 * dof) {
+        mqd = fmaxf(mqd, fabsf(v));
+      } else {
+        const int j = kf - 2 * dof;
+        sc5[0] = j == 0 ? v : sc5[0];
+        sc5[1] = j == 1 ? v : sc5[1];
+        sc5[2] = j == 2 ? v : sc5[2];
+        sc5[3] = j == 3 ? v : sc5[3];
+        sc5[4] = j == 4 ? v : sc5[4];
+      }
+    }
+    // cum / dist from the pre-draws (lanes 0 and adv), identical on all lanes
     if (adv) {
-      s.cum = __dadd_rn(s.cum, __dmul_rn(__dmul_rn(head, 0.05), env_rand(mt, idx, 0, so, ss)));
-      j = 2;
+      const double rc = __shfl_sync(qmask, r_pre, qbase);
+      s.cum = __dadd_rn(s.cum, __dmul_rn(__dmul_rn(head, 0.05), rc));
     }
     if (a == TL_EV_EXCESSIVE_COLLISIONS) s.cum = z.L105;                 // synth.py:210-213
     if (app) {
-      const double r = env_rand(mt, idx, j, so, ss);
-      s.dist = a == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, r) : uniform_rn(0.3, 0.8, r);
-      j += 2;
+      const double rd = __shfl_sync(qmask, r_pre, qbase + adv);
+      s.dist = a == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rd) : uniform_rn(0.3, 0.8, rd);
     }
     s.t += 1;
-    uint32_t ind, err;
-    env_emit<DOFMAX>(p, s, z, c, mt, idx, j, so, ss, col, ind, err);
-    const uint32_t m = edge_mask(c.subtask, s.prev_ind, ind);
-    env_fold(s, m, err);
-    s.prev_ind = ind;
-    if (p.step_mask) p.step_mask[col] = (uint8_t)m;
+    const float vdist = z.has_goal ? __double2float_rn(s.dist) : fnan;
+    const float vforce = z.has_force ? __double2float_rn(s.force) : fnan;
+    const float vcum = __double2float_rn(s.cum);
+    const float vart = z.has_art ? __double2float_rn(s.art) : fnan;
+    {
+      const int f = 2 * dof + 5 + q;  // dist, force, cum, art: one plane per lane
+      p.obs[(int64_t)f * st + col] = q == 0 ? vdist : q == 1 ? vforce : q == 2 ? vcum : vart;
+    }
+    // gather the record's predicate inputs on lane 0
+    mq = fmaxf(mq, __shfl_xor_sync(qmask, mq, 1));
+    mq = fmaxf(mq, __shfl_xor_sync(qmask, mq, 2));
+    mqd = fmaxf(mqd, __shfl_xor_sync(qmask, mqd, 1));
+    mqd = fmaxf(mqd, __shfl_xor_sync(qmask, mqd, 2));
+    if (!c.rest_zero) {
+      md = fmax(md, __shfl_xor_sync(qmask, md, 1));
+      md = fmax(md, __shfl_xor_sync(qmask, md, 2));
+    }
+    float sv[5];
+#pragma unroll
+    for (int j = 0; j < 5; j++) sv[j] = __shfl_sync(qmask, sc5[j], qbase + ((pre + 2 * dof + j) & 3));
+    if (q == 0) {
+      if (p.obs_grasped) p.obs_grasped[col] = s.grasped;
+      RecV<float> v;
+      v.tor = sv[0]; v.vx = sv[1]; v.vy = sv[2]; v.om = sv[3]; v.der = sv[4];
+      v.dist = vdist; v.force = vforce; v.cum = vcum; v.art = vart;
+      v.g = s.grasped != 0;
+      v.jm = mq; v.qdm = mqd; v.jm_d = md;
+      uint32_t ind, err;
+      record_bits(c, v, s.sc_ru, s.sc_d, ind, err);
+      const uint32_t m = edge_mask(c.subtask, s.prev_ind, ind);
+      env_fold(s, m, err);
+      s.prev_ind = ind;
+      if (p.step_mask) p.step_mask[col] = (uint8_t)m;
+    }
   }
   cp_async_wait<0>();
-  env_store(&p.st[e], s);
+  if (q == 0) env_store(&p.st[e], s);
 }
 
 // labels of the episodes so far (classify(extract_events(records[0..t])))

@@ -470,13 +470,13 @@ int tl_env_step(void* state, int32_t n_env, int32_t dof, const uint8_t* actions,
   ep.obs_stride = obs_stride;
   ep.obs_grasped = obs_grasped;
   ep.step_mask = step_mask;
-  const int grid = (n_env + kEnvThreads - 1) / kEnvThreads;
+  const int grid = (n_env + kEnvQPerBlock - 1) / kEnvQPerBlock;
   if (dof <= 7) {
-    set_max_smem(k_env_step<7>, (int)sizeof(EnvSmem<7>));
-    k_env_step<7><<<grid, kEnvThreads, sizeof(EnvSmem<7>), S(stream)>>>(ep);
+    set_max_smem(k_env_step<7>, (int)sizeof(EnvQSmem<7>));
+    k_env_step<7><<<grid, kEnvQThreads, sizeof(EnvQSmem<7>), S(stream)>>>(ep);
   } else {
-    set_max_smem(k_env_step<16>, (int)sizeof(EnvSmem<16>));
-    k_env_step<16><<<grid, kEnvThreads, sizeof(EnvSmem<16>), S(stream)>>>(ep);
+    set_max_smem(k_env_step<16>, (int)sizeof(EnvQSmem<16>));
+    k_env_step<16><<<grid, kEnvQThreads, sizeof(EnvQSmem<16>), S(stream)>>>(ep);
   }
   return check_launch();
 }
