@@ -351,6 +351,19 @@ int tl_compact_records(const tl_records* src, int32_t n_env,
 int tl_mode_histogram(const tl_label* labels, int32_t n, int64_t* hist,
                       void* stream);
 
+/* ---- analytics counting (analytics.py:121-160, :279-298) ----------------
+ * counts[g*42 + c] over the valid labels (status 0) of group g (group NULL =
+ * one group): c < 39 mode id, 39 success_once, 40 success_at_end, 41 labels.
+ * Zeroed by the call.  The host derives SoR/SaeR/FR and the per-mode
+ * fractions exactly as mode_table does. */
+int tl_group_mode_counts(const tl_label* labels, const int32_t* group, int64_t n,
+                         int32_t n_groups, int64_t* counts, void* stream);
+/* progressive_completion: slot_label[c*n_slots + k] = label index of chain
+ * c's slot k, or -1 for an auto-success slot.  alive[k] = chains whose
+ * bound slots 0..k all have success_once (status 0).  n_slots <= 64. */
+int tl_chain_progress(const tl_label* labels, const int64_t* slot_label, int64_t n_chain,
+                      int32_t n_slots, int64_t* alive, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

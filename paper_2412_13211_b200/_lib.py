@@ -167,6 +167,8 @@ def lib():
         "tl_env_step": ([vp, i32, i32, vp, i32, vp, i64, vp, vp, vp], ctypes.c_int),
         "tl_env_labels": ([vp, i32, vp, vp, vp, vp], ctypes.c_int),
         "tl_env_script_actions": ([vp, vp, vp, i32, i32, i32, vp, vp], ctypes.c_int),
+        "tl_group_mode_counts": ([vp, vp, i64, i32, vp, vp], ctypes.c_int),
+        "tl_chain_progress": ([vp, vp, i64, i32, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -186,7 +188,8 @@ def exported_symbols():
             "tl_mode_histogram", "tl_eval_predicates", "tl_scan_counts",
             "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes",
             "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
-            "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions"]
+            "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions",
+            "tl_group_mode_counts", "tl_chain_progress"]
 
 
 def check(rc, what):

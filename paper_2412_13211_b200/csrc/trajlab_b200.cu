@@ -1,5 +1,6 @@
 // trajlab_b200.cu -- C ABI of libtrajlab_b200.so (see include/trajlab_b200.h).
 // Single translation unit: kernels live in the tl_*.cuh headers.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include "tl_synth_cta.cuh"
 #include "tl_filter.cuh"
 #include "tl_env.cuh"
+#include "tl_analytics.cuh"
 
 namespace {
 
@@ -501,6 +503,33 @@ int tl_env_script_actions(const tl_script* scripts, const uint8_t* step_kind,
   if (n_env == 0 || k_steps == 0) return TL_OK;
   k_env_script_actions<<<(n_env + 127) / 128, 128, 0, S(stream)>>>(scripts, step_kind, step_gap,
                                                                   n_env, t0, k_steps, actions);
+  return check_launch();
+}
+
+// ---- analytics counting ------------------------------------------------------
+int tl_group_mode_counts(const tl_label* labels, const int32_t* group, int64_t n,
+                         int32_t n_groups, int64_t* counts, void* stream) {
+  if (!labels || !counts || n < 0 || n_groups < 1) return TL_E_INVALID;
+  const size_t bytes = (size_t)n_groups * kCountCols * sizeof(int64_t);
+  if (cudaMemsetAsync(counts, 0, bytes, S(stream))) return TL_E_CUDA;
+  if (n == 0) return TL_OK;
+  const int cells = n_groups * kCountCols;
+  const int use_smem = cells <= 8192;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 4);
+  k_group_counts<<<grid, 256, use_smem ? cells * 4 : 0, S(stream)>>>(
+      labels, group, n, n_groups, reinterpret_cast<unsigned long long*>(counts), use_smem);
+  return check_launch();
+}
+
+int tl_chain_progress(const tl_label* labels, const int64_t* slot_label, int64_t n_chain,
+                      int32_t n_slots, int64_t* alive, void* stream) {
+  if (!labels || !slot_label || !alive || n_chain < 0 || n_slots < 1 || n_slots > 64)
+    return TL_E_INVALID;
+  if (cudaMemsetAsync(alive, 0, (size_t)n_slots * sizeof(int64_t), S(stream))) return TL_E_CUDA;
+  if (n_chain == 0) return TL_OK;
+  const int grid = (int)std::min<int64_t>((n_chain + 255) / 256, (int64_t)sm_count() * 4);
+  k_chain_alive<<<grid, 256, 0, S(stream)>>>(labels, slot_label, n_chain, n_slots,
+                                            reinterpret_cast<unsigned long long*>(alive));
   return check_launch();
 }
 
