@@ -284,6 +284,102 @@ def env_api_run(dev, stream, n_env=4096, T=200, reps=10):
     return res
 
 
+def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
+    """C5: 1M synthetic episodes (fuzz, 250k per subtask, default
+    FuzzConfig) labelled, all-gathered in episode order (N>1) and filtered
+    with the A.6.1 recipe, quota 1000 per target_id = seed % 9.
+    Whole pipeline timed on the device (max over ranks); labels/s is the
+    BASELINE 'labelled trajectories/sec'."""
+    import torch
+    import paper_2412_13211_b200 as P
+    from paper_2412_13211_b200 import dist as D
+    spec = P.FilterSpec(allow=[
+        P.AllowRule("Pick", frozenset({"pick.s1_straightforward"}), 1.0),
+        P.AllowRule("Place", frozenset({"place.s1_place_in_goal"}), 0.5),
+        P.AllowRule("Place", frozenset({"place.s2_drop_to_goal"}), 0.5),
+        P.AllowRule("Open", frozenset({"open.s1_open"}), 1.0),
+        P.AllowRule("Close", frozenset({"close.s1_close"}), 1.0)], quota_per_target=1000)
+    ms = []
+    man = None
+    for k in range(reps + 1):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        labels, man, _ = D.fuzz_label_filter_sharded(n_per_subtask, spec)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k:
+            ms.append(a.elapsed_time(b))
+    t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    t = float(t.item()) / 1e3
+    n_total = 4 * n_per_subtask
+    return {"workload": "C5: fuzz 4 x 250k episodes (default FuzzConfig) -> label -> "
+                        "all-gather -> filter_labels (A.6.1 recipe, quota 1000/target)",
+            "episodes": n_total, "n_gpus": world, "ms": 1e3 * t,
+            "labelled_trajectories_per_s": n_total / t,
+            "selected": int(sum(man.pool_selected)), "pools": len(man.pools),
+            "timing": "CUDA events around the whole pipeline (incl. host glue), max over ranks"}
+
+
+def c4_run(dev, stream, world, n_chain=4096, reps=3):
+    """C4: SetTable chains, 4096 per GPU; chain c runs Open,
+    Pick, Place, Close twice with seeds 8c + k (k = 0..7); slot success =
+    success_once; progressive_completion over the 16-slot settable plan
+    (alive counts all-reduced over ranks)."""
+    import torch
+    import paper_2412_13211_b200 as P
+    from paper_2412_13211_b200 import _lib as L, core
+    from paper_2412_13211_b200.analytics import BUILTIN_PLANS
+    rank = torch.distributed.get_rank() if world > 1 else 0
+    plan = BUILTIN_PLANS["settable"]
+    c0 = rank * n_chain
+    cfg = P.FuzzConfig()
+    cs = core.synth_csets(P.Thresholds()).to_device(dev)
+    order = {"Open": 0, "Pick": 1, "Place": 2, "Close": 3}   # k within a repetition
+    sub_idx = {"Pick": 0, "Place": 1, "Open": 2, "Close": 3}
+    chains = torch.arange(c0, c0 + n_chain, dtype=torch.int64, device=dev)
+    # slot -> (subtask, repetition); label rows: block per (subtask, repetition)
+    slot_label = torch.full((n_chain, len(plan)), -1, dtype=torch.int64, device=dev)
+    blocks = []
+    for j, slot in enumerate(plan.slots):
+        if slot.auto_success:
+            continue
+        rep = 0 if j < 8 else 1
+        blocks.append((j, slot.subtask, rep))
+    seeds_by_block = [(8 * chains + 4 * rep + order[sub]) for (_, sub, rep) in blocks]
+    for bi, (j, _, _) in enumerate(blocks):
+        slot_label[:, j] = bi * n_chain + torch.arange(n_chain, device=dev)
+    alive = torch.empty(len(plan), dtype=torch.int64, device=dev)
+    ms = []
+    for k in range(reps + 1):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        labs = [core.fuzz_batch(sd, sub_idx[sub], cfg, P.Thresholds(), cs).labels[:n_chain]
+                for sd, (_, sub, _) in zip(seeds_by_block, blocks)]
+        lab = torch.cat(labs)
+        L.check(L.lib().tl_chain_progress(L.ptr(lab), L.ptr(slot_label), n_chain, len(plan),
+                                          L.ptr(alive), L.stream_ptr()), "chain")
+        if world > 1:
+            torch.distributed.all_reduce(alive)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k:
+            ms.append(a.elapsed_time(b))
+    t = sum(ms) / len(ms) / 1e3
+    curve = [100.0 * int(x) / (n_chain * world) for x in alive.cpu().tolist()]
+    return {"workload": "C4: SetTable chains (settable plan, 16 slots), 4096 chains/GPU, "
+                        "8 fuzz episodes per chain (seeds 8c+k), progressive_completion",
+            "chains_per_gpu": n_chain, "n_gpus": world, "ms": 1e3 * t,
+            "chains_per_s": n_chain * world / t,
+            "labelled_trajectories_per_s": 8 * n_chain * world / t,
+            "progressive_completion": curve}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -462,6 +558,8 @@ def main():
         # ---- sizing run: k_label over 2^19 x 200-step episodes
         sizing = label_sizing_run(L, core, lib, dev, stream, flush)
         env_api = env_api_run(dev, stream)
+        c5 = c5_run(dev, stream, world)
+        c4 = c4_run(dev, stream, world)
     clk = clocks.summary()
 
     recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
@@ -524,6 +622,8 @@ def main():
                                          "generated record (93 B/env-step)"}},
         "label_sizing": sizing,
         "env_api": env_api,
+        "c5": c5,
+        "c4": c4,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
                          "sample": cb_sample, "trajectories_per_sec": cb_eps},
         "clocks": clk,

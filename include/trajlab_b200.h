@@ -310,6 +310,15 @@ int tl_env_script_actions(const tl_script* scripts, const uint8_t* step_kind,
                           const int32_t* step_gap, int32_t n_env, int32_t t0,
                           int32_t k_steps, uint8_t* actions, void* stream);
 
+/* filter_buckets on the device (pipeline.py:276-304) for labels already in
+ * episode_id order: bucket[i] = pool_b0[pool[key[i]*4 + subtask]] +
+ * rule_lut[subtask*39 + mode] (position of the first allow rule of the
+ * subtask containing the mode, -1 none); -1 for invalid labels, unmatched
+ * modes or pool < 0.  Feeds tl_filter_select. */
+int tl_filter_buckets(const tl_label* labels, const int32_t* key, int64_t n,
+                      const int8_t* rule_lut, const int32_t* pool, const int32_t* pool_b0,
+                      int32_t n_keys, int32_t* bucket, void* stream);
+
 /* K5: filter_labels selection (pipeline.py:276-338).  Labels are already
  * in episode_id order.  bucket[i] in [-1, n_buckets): the (quota key,
  * subtask) pool's allow-rule position the label falls into (-1 = none).

@@ -169,6 +169,7 @@ def lib():
         "tl_env_script_actions": ([vp, vp, vp, i32, i32, i32, vp, vp], ctypes.c_int),
         "tl_group_mode_counts": ([vp, vp, i64, i32, vp, vp], ctypes.c_int),
         "tl_chain_progress": ([vp, vp, i64, i32, vp, vp], ctypes.c_int),
+        "tl_filter_buckets": ([vp, vp, i64, vp, vp, vp, i32, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -189,7 +190,7 @@ def exported_symbols():
             "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes",
             "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
             "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions",
-            "tl_group_mode_counts", "tl_chain_progress"]
+            "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets"]
 
 
 def check(rc, what):

@@ -85,4 +85,28 @@ __global__ void k_chain_alive(const tl_label* __restrict__ labels,
     if (h[k]) atomicAdd(&alive[k], (unsigned long long)h[k]);
 }
 
+// filter_labels bucket encoding on the device (pipeline.py:276-304): label
+// i of subtask s with quota key k goes to bucket pool_b0[pool[k*4+s]] +
+// rule_lut[s*39 + mode] (first allow rule of s containing its mode), or
+// -1 when no rule matches / the pool does not exist / the label is invalid.
+__global__ void k_filter_buckets(const tl_label* __restrict__ labels,
+                                 const int32_t* __restrict__ key, int64_t n,
+                                 const int8_t* __restrict__ rule_lut,
+                                 const int32_t* __restrict__ pool,
+                                 const int32_t* __restrict__ pool_b0, int n_keys,
+                                 int32_t* __restrict__ bucket) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const tl_label L = labels[i];
+    int b = -1;
+    const int k = key[i];
+    if (L.status == 0 && L.mode < 39 && L.subtask < 4 && k >= 0 && k < n_keys) {
+      const int r = rule_lut[L.subtask * 39 + L.mode];
+      const int pl = pool[k * 4 + L.subtask];
+      if (r >= 0 && pl >= 0) b = pool_b0[pl] + r;
+    }
+    bucket[i] = b;
+  }
+}
+
 }  // namespace tl

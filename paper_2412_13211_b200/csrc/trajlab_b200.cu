@@ -533,6 +533,18 @@ int tl_chain_progress(const tl_label* labels, const int64_t* slot_label, int64_t
   return check_launch();
 }
 
+int tl_filter_buckets(const tl_label* labels, const int32_t* key, int64_t n,
+                      const int8_t* rule_lut, const int32_t* pool, const int32_t* pool_b0,
+                      int32_t n_keys, int32_t* bucket, void* stream) {
+  if (!labels || !key || !rule_lut || !pool || !pool_b0 || !bucket || n < 0 || n_keys < 1)
+    return TL_E_INVALID;
+  if (n == 0) return TL_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
+  k_filter_buckets<<<grid, 256, 0, S(stream)>>>(labels, key, n, rule_lut, pool, pool_b0, n_keys,
+                                               bucket);
+  return check_launch();
+}
+
 size_t tl_filter_scratch_bytes(int64_t n, int32_t n_buckets, int32_t n_pools) {
   const int64_t tiles = (n + kFilterTile - 1) / kFilterTile;
   const size_t a = (size_t)(tiles > 0 ? tiles : 1) * (size_t)(n_buckets > 0 ? n_buckets : 1) * 4;

@@ -98,3 +98,23 @@ def fuzz_label_sharded(n_total: int, subtask: int, cfg, th=None, group=None, see
     else:
         all_labels = sb.labels[:hi - lo]
     return ShardResult(sb.labels[:hi - lo], all_labels, hist, lo, hi)
+
+
+def fuzz_label_filter_sharded(n_per_subtask: int, spec, cfg=None, n_targets: int = 9,
+                              th=None, group=None):
+    """C5: fuzz(seed, kind) for seeds [0, n) of every subtask,
+    seed-sharded over the ranks, labels all-gathered in rank (= episode_id)
+    order, target_id = f"{seed % n_targets:03d}", then filter_labels on every
+    rank's GPU (identical, deterministic manifests).  Returns (labels
+    [4n, 24] in SUBTASK_ORDER blocks, DeviceManifest, key names)."""
+    import torch
+    from . import _lib as L
+    from .pipeline import filter_labels_device
+    from .synth import FuzzConfig
+    cfg = cfg or FuzzConfig()
+    dev = L.device()
+    parts = [fuzz_label_sharded(n_per_subtask, s, cfg, th, group).all_labels for s in range(4)]
+    labels = torch.cat(parts)
+    keys = (torch.arange(n_per_subtask, dtype=torch.int32, device=dev) % n_targets).repeat(4)
+    names = [f"{t:03d}" for t in range(n_targets)]
+    return labels, filter_labels_device(labels, keys, names, spec), names

@@ -271,3 +271,37 @@ def test_filter_semantics():
                         T.FilterSpec([T.AllowRule("Pick", frozenset({"pick.s1_straightforward"}), 1.0)],
                                      quota_per_target=10))
     assert len(m.entries) == 15 and len(m.shortfalls) == 1
+
+
+def test_c5_device_filter_matches_host_filter():
+    """C5 shape at small scale: device bucket encoding + selection + counts
+    == filter_labels over the equivalent LabelRecords (host buckets, pinned
+    to the reference's filter fixtures)."""
+    import numpy as np
+    import paper_2412_13211_b200 as P
+    from paper_2412_13211_b200 import _lib as L, dist as D
+    from paper_2412_13211_b200.modes import MODE_LIST
+    from paper_2412_13211_b200.model import SUBTASK_ORDER
+    spec = P.FilterSpec(allow=[
+        P.AllowRule("Pick", frozenset({"pick.s1_straightforward"}), 1.0),
+        P.AllowRule("Place", frozenset({"place.s1_place_in_goal"}), 0.5),
+        P.AllowRule("Place", frozenset({"place.s2_drop_to_goal"}), 0.5),
+        P.AllowRule("Open", frozenset({"open.s1_open"}), 1.0),
+        P.AllowRule("Close", frozenset({"close.s1_close"}), 1.0)], quota_per_target=25)
+    n = 1500
+    labels, man, names = D.fuzz_label_filter_sharded(n, spec, n_targets=9)
+    lab = labels.cpu().numpy().reshape(-1).view(L.LABEL_DTYPE)
+    recs = []
+    for s, kind in enumerate(SUBTASK_ORDER):
+        for seed in range(n):
+            r = lab[s * n + seed]
+            assert r["status"] == 0
+            recs.append(P.LabelRecord(
+                episode_id=f"fuzz-{kind.value.lower()}-{seed:08d}", subtask=kind.value,
+                mode_id=MODE_LIST[r["mode"]], success_once=bool(r["flags"] & 1),
+                success_at_end=bool(r["flags"] & 2), target_id=f"{seed % 9:03d}"))
+    want = P.filter_labels(recs, spec)
+    got_ids = sorted(recs[i].episode_id for i in man.selected_rows())
+    assert got_ids == [e.episode_id for e in want.entries]
+    assert man.counts == want.counts
+    assert man.shortfalls == want.shortfalls
