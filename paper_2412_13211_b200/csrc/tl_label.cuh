@@ -129,6 +129,21 @@ __device__ __forceinline__ void record_bits(const tl_cset& c, const RecV<T>& v,
   if (succ) ind |= IND_SUCCESS;
 }
 
+// record_bits split at cum_robot_force: the bits computed with `over` =
+// false (cum_patch_bits then applies the real cum).  Exact because every
+// success / ERR_SUCC condition of record_bits is conjoined with !over and
+// the cum bits depend on nothing else.
+__device__ __forceinline__ uint32_t cum_patch_bits(const tl_cset& c, float cum, uint32_t ind,
+                                                   uint32_t& err) {
+  const bool over = GT(cum, c.rd_limit, c.limit);
+  if (over) {
+    ind &= ~IND_SUCCESS;
+    err &= ~ERR_SUCC;
+  }
+  return (ind & ~(IND_CUM_LE | IND_CUM_GT)) | (LE(cum, c.rd_limit, c.limit) ? IND_CUM_LE : 0u) |
+         (over ? IND_CUM_GT : 0u);
+}
+
 // edge tests of extract_events in EVENT_ORDER bit order
 __device__ __forceinline__ uint32_t edge_mask(int subtask, uint32_t p, uint32_t c) {
   const uint32_t rise = ~p & c, fall = p & ~c;

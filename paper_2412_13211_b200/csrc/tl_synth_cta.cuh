@@ -1,4 +1,4 @@
-// tl_synth_cta.cuh -- realize + online labelling with one 4-warp CTA per
+// tl_synth_cta.cuh -- realize + online labelling with one 3-warp CTA per
 // episode (the latency-optimised form of k_synth).
 //
 // Same semantics as k_synth (tl_synth.cuh; reference synth.py:100-348 +
@@ -11,15 +11,18 @@
 //   * the serial f64 cum_robot_force recurrence runs on warp 0, eight
 //     records per group of vector shared-memory loads, split at the
 //     ExcessiveCollisions record (before it every step draws, after it cum
-//     is constant);
-//   * each warp folds its 32 event masks into a partial label state,
-//     combined in order by warp 0.
+//     is constant), CONCURRENTLY with the emission of the same wave by
+//     warps 1-2 (one record per thread); the cum-dependent label bits are
+//     patched in afterwards (cum_patch_bits);
+//   * each emission warp folds its 32 event masks into a partial label
+//     state, combined in order by warp 0.
 #pragma once
 #include "tl_synth.cuh"
 
 namespace tl {
 
-constexpr int kCtaThreads = 64;
+constexpr int kWave = 64;                  // records per wave (warps 1-2)
+constexpr int kCtaThreads = kWave + 32;    // + warp 0 (cum chain)
 
 template <int DOFMAX>
 struct CtaCfg {
@@ -37,12 +40,11 @@ struct CtaSmem {
   int32_t hw[kMaxSteps + 1];
   StepSt st[kMaxSteps + 1];
   double dist_after[kMaxSteps];
-  double radv[kCtaThreads];
-  float cum32[kCtaThreads];
-  uint32_t ind[kCtaThreads];
-  uint32_t emask[kCtaThreads];
-  uint32_t eerr[kCtaThreads];
-  LState part[kCtaThreads / 32];
+  double radv[kWave];
+  float cum32[kWave];
+  uint32_t ind[kWave];      // indicator bits without the cum patch
+  uint32_t eerr[kWave];
+  LState part[kWave / 32];
   uint8_t kind[kMaxSteps];
   uint8_t sflag[kMaxSteps];
   int32_t misc[16];
@@ -93,18 +95,20 @@ __device__ __forceinline__ void mt_twist_block(uint32_t* mt, uint32_t* ring, uin
   twist_phase4<DOFMAX, 112, 156>(mt, ring, base);
 }
 
-__device__ __forceinline__ int block_max2(int v, int32_t* red) {
+__device__ __forceinline__ int block_max(int v, int32_t* red) {
   const int warp = threadIdx.x >> 5;
   v = __reduce_max_sync(kFull, v);
   if (lane_id() == 0) red[warp] = v;
   __syncthreads();
-  const int m = max(red[0], red[1]);
+  int m = red[0];
+#pragma unroll
+  for (int w = 1; w < kCtaThreads / 32; w++) m = max(m, red[w]);
   __syncthreads();
   return m;
 }
 
 template <bool FUZZ, int DOFMAX>
-__global__ void __launch_bounds__(kCtaThreads)
+__global__ void __launch_bounds__(kCtaThreads, 7)
     k_synth_cta(SynthParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CtaSmem<DOFMAX>& S = *reinterpret_cast<CtaSmem<DOFMAX>*>(smem_raw);
@@ -248,9 +252,11 @@ __global__ void __launch_bounds__(kCtaThreads)
       else if (last_window) r_end = n_rec;
       else r_end = S.misc[3] + 1;
       int seg_hint = 0;
-      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += kCtaThreads) {
-        const int r = r0 + tid;
-        const bool valid = r < r_end;
+      const bool emitter = warp > 0;
+      const int et = tid - 32;  // record slot of an emission thread
+      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += kWave) {
+        const int r = r0 + et;
+        const bool valid = emitter && r < r_end;
         int o = 0, adv = 0, app = 0, emit = 0, sidx = 0, ev = -1, s = 0;
         if (valid) {
           if (r == 0) {
@@ -275,9 +281,9 @@ __global__ void __launch_bounds__(kCtaThreads)
             }
           }
         }
-        if (tid == 0) S.misc[12] = s;
+        if (et == 0) S.misc[12] = s;
         const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
-        const int need_max = block_max2(need, S.red);  // also publishes misc[12]
+        const int need_max = block_max(need, S.red);  // also publishes misc[12]
         seg_hint = S.misc[12];
         const int wbase = 20 + 8 * min(wave_no, 12);  // profiling build only
         if (tid == 0 && e == 0) TL_STAMP(wbase);
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(kCtaThreads)
           return rand53(wv.x, wv.y);
         };
         int my_err = 0;
-        S.radv[tid] = valid && adv ? rnd(o) : 0.0;
+        if (emitter) S.radv[et] = valid && adv ? rnd(o) : 0.0;
         if (valid && app) {
           const double rr = rnd(o + 2 * adv);
           S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rr) : uniform_rn(0.3, 0.8, rr);
@@ -317,11 +323,21 @@ __global__ void __launch_bounds__(kCtaThreads)
         }
         if (valid && perr && ev >= 0 && s == pstep && !my_err) my_err = perr;
         if (my_err) atomicMin(&S.misc[13], ((s_base + s) << 8) | my_err);
-        const int cnt = min(kCtaThreads, r_end - r0);
-        // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213)
-        // on warp 0.  Record 0 never draws; every later record draws until
-        // the ExcessiveCollisions record, which jumps to 1.05*limit for good.
-        if (warp == 0) {
+        __syncthreads();
+        {
+          const int ek = S.misc[13];
+          if (ek != 0x7fffffff) {
+            err_code = ek & 0xff;
+            err_step = ek >> 8;
+            break;
+          }
+        }
+        const int cnt = min(kWave, r_end - r0);
+        if (!emitter) {
+          // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213),
+          // overlapped with the emission below.  Record 0 never draws; every
+          // later record draws until the ExcessiveCollisions record, which
+          // jumps to 1.05*limit for good.
           const int jx = exc_rec >= r0 ? min(cnt, exc_rec - r0) : 0;  // draws in [j0, jx)
           int j = 0;
           if (r0 == 0) {
@@ -354,18 +370,9 @@ __global__ void __launch_bounds__(kCtaThreads)
             const float c105 = __double2float_rn(cum);
             for (int k = max(j, 0) + lane; k < cnt; k += 32) S.cum32[k] = c105;
           }
-        }
-        __syncthreads();
-        if (tid == 0 && e == 0) TL_STAMP(wbase + 3);
-        const int ek = S.misc[13];
-        if (ek != 0x7fffffff) {
-          err_code = ek & 0xff;
-          err_step = ek >> 8;
-          break;
-        }
-        // ---- emit + write + per-record indicator bits ----------------------------
-        uint32_t ind = 0, errb = 0;
-        if (valid) {
+        } else if (valid) {
+          // ---- emit + write + indicator bits (cum patched after the barrier) ----
+          uint32_t ind = 0, errb = 0;
           const int64_t rr = rs + r;
           const StepSt stv = S.st[sidx];
           const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(kCtaThreads)
           v.der = draw(k2 + 4, 0.2, 1.0);
           v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
           v.force = stv.force;
-          v.cum = S.cum32[tid];
+          v.cum = 0.f;  // over = false here; cum_patch_bits applies the real value
           v.art = stv.art;
           v.g = stv.grasped != 0;
           v.qdm = mqd;
@@ -417,28 +424,43 @@ __global__ void __launch_bounds__(kCtaThreads)
           dst[4 * stride] = v.der;
           dst[5 * stride] = v.dist;
           dst[6 * stride] = v.force;
-          dst[7 * stride] = v.cum;
           dst[8 * stride] = v.art;
           p.out.grasped[rr] = (uint8_t)v.g;
           record_bits(c, v, sc_ru, sc_d, ind, errb);
+          S.ind[et] = ind;
+          S.eerr[et] = errb;
         }
-        S.ind[tid] = ind;
         __syncthreads();
-        if (tid == 0 && e == 0) TL_STAMP(wbase + 4);
-        const uint32_t prev = tid ? S.ind[tid - 1] : ind_carry;
-        const uint32_t mask = (valid && r > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
-        if (valid && p.step_mask) p.step_mask[rs + r] = (uint8_t)mask;
-        ind_carry = S.ind[cnt - 1];
-        {  // per-warp partial fold, combined in record order by warp 0
+        if (tid == 0 && e == 0) TL_STAMP(wbase + 3);
+        if (emitter) {
+          uint32_t ind = 0, errb = 0, prev = ind_carry;
+          if (valid) {
+            const float cm = S.cum32[et];
+            P[rs + r + (int64_t)(2 * dof + 7) * stride] = cm;  // cum_robot_force plane
+            errb = S.eerr[et];
+            ind = cum_patch_bits(c, cm, S.ind[et], errb);
+            if (et > 0) {
+              uint32_t e2 = 0;
+              prev = cum_patch_bits(c, S.cum32[et - 1], S.ind[et - 1], e2);
+            }
+          }
+          const uint32_t mask = (valid && r > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
+          if (valid && p.step_mask) p.step_mask[rs + r] = (uint8_t)mask;
+          // per-warp partial fold, combined in record order by warp 0
           LState part;
           lstate_init(part);
           lstate_fold(part, mask, valid ? errb : 0u);
-          if (lane == 0) S.part[warp] = part;
+          if (lane == 0) S.part[warp - 1] = part;
+        }
+        // indicator bits of the wave's last record (carry into the next wave)
+        {
+          uint32_t e2 = 0;
+          ind_carry = cum_patch_bits(c, S.cum32[cnt - 1], S.ind[cnt - 1], e2);
         }
         __syncthreads();
         if (warp == 0) {
 #pragma unroll
-          for (int w = 0; w < kCtaThreads / 32; w++) {
+          for (int w = 0; w < kWave / 32; w++) {
             const LState& q = S.part[w];
 #pragma unroll
             for (int k = 0; k < 7; k++)

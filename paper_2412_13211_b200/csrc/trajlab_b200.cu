@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -270,6 +271,9 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCtaThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
+  if (getenv("TL_DEBUG"))
+    fprintf(stderr, "k_synth_cta: %d CTAs/SM (smem %d B, %d threads), grid %d\n", per_sm, smem,
+            kCtaThreads, grid);
   k<<<grid, kCtaThreads, smem, S(stream)>>>(sp);
   return check_launch();
 }

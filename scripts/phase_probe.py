@@ -32,5 +32,5 @@ for w in range(8):
     b = 20 + 8 * w
     if t[b] == 0 or t[b+5] < t[b]: break
     prev = t[12] if w == 0 else t[b - 3]
-    print(f" wave {w}: desc {t[b]-prev}  twist {t[b+1]-t[b]}  draws {t[b+2]-t[b+1]}  cum {t[b+3]-t[b+2]}  emit {t[b+4]-t[b+3]}  fold {t[b+5]-t[b+4]}")
+    print(f" wave {w}: desc {t[b]-prev}  twist {t[b+1]-t[b]}  draws {t[b+2]-t[b+1]}  cum||emit {t[b+3]-t[b+2]}  patch+fold {t[b+5]-t[b+3]}")
 print("env0 total %d cycles; CTA0 second env done at +%d" % (t[13]-t[10], t[14]-t[10] if t[14] else -1))
