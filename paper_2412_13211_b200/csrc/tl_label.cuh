@@ -421,6 +421,27 @@ __device__ __forceinline__ void close_cut(const tl_cset& c, double a0, float& ru
   ru = __double2float_ru(d);
 }
 
+// planes the subtask's predicates read, in buffer order:
+// q[dof], qd[dof], v_x, v_y, omega, dist_ee_rest, cum, then
+// Pick: force | Place: q_tor, dist_obj_goal | Open/Close: q_tor, force, art
+__device__ __forceinline__ int tma_nplanes(int sub, int dof) {
+  return 2 * dof + (sub == TL_PICK ? 6 : sub == TL_PLACE ? 7 : 8);
+}
+__device__ __forceinline__ int tma_plane(int sub, int dof, int p) {
+  const int f0 = 2 * dof;
+  if (p < f0) return p;
+  switch (p - f0) {
+    case 0: return f0 + 1;  // v_base_x
+    case 1: return f0 + 2;  // v_base_y
+    case 2: return f0 + 3;  // omega_base
+    case 3: return f0 + 4;  // dist_ee_rest
+    case 4: return f0 + 7;  // cum_robot_force
+    case 5: return sub == TL_PICK ? f0 + 6 : f0;  // force | q_tor
+    case 6: return sub == TL_PLACE ? f0 + 5 : f0 + 6;  // dist_obj_goal | force
+    default: return f0 + 8;  // art_q
+  }
+}
+
 // ---- K1 vector path: 4 consecutive records per lane ----------------------------
 __device__ __forceinline__ float4 ldf4(const float* p) {
   return __ldcs(reinterpret_cast<const float4*>(p));  // streamed once: evict-first
@@ -542,6 +563,73 @@ __device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, i
   }
 }
 
+// one record per lane (any layout, f32 or f64 records, any rest posture)
+template <typename T, int DOFMAX>
+__device__ __forceinline__ void label_scalar(const tl_records& R, const tl_cset& c, int64_t rs, int n,
+                                             float sc_ru, double sc_d, LState& S,
+                                             uint8_t* step_mask, uint8_t* step_success) {
+  const int lane = lane_id();
+  const T* __restrict__ P = reinterpret_cast<const T*>(R.planes);
+  const int64_t stride = R.plane_stride;
+  const int dof = R.dof;
+  const int f0 = 2 * dof;
+  for (int t0 = 0; t0 < n; t0 += 32) {
+    const int t = t0 + lane;
+    const bool valid = t < n;
+    const int64_t r = rs + t;
+    RecV<T> v;
+    uint32_t ind = 0, err = 0;
+    if (valid) {
+      v.der = P[(f0 + 4) * stride + r];
+      v.cum = P[(f0 + 7) * stride + r];
+      v.vx = P[(f0 + 1) * stride + r];
+      v.vy = P[(f0 + 2) * stride + r];
+      v.om = P[(f0 + 3) * stride + r];
+      // Python-max of |q_i - rest_i| and of |qd_i|
+      T m = 0, mq = 0;
+      double md = 0.0;
+#pragma unroll
+      for (int i = 0; i < DOFMAX; i++) {
+        if (i < dof) {
+          const T q = P[i * stride + r];
+          const T qd = P[(dof + i) * stride + r];
+          const T aq = tabs(q), aqd = tabs(qd);
+          m = i == 0 ? aq : pymax_step(m, aq);
+          mq = i == 0 ? aqd : pymax_step(mq, aqd);
+          if (!c.rest_zero) {
+            const double dv = fabs(__dsub_rn((double)q, c.rest_arm[i]));
+            md = i == 0 ? dv : pymax_step(md, dv);
+          }
+        }
+      }
+      v.jm = m;
+      v.qdm = mq;
+      v.jm_d = md;
+      v.tor = 0; v.dist = 0; v.force = 0; v.art = 0; v.g = false;
+      if (c.subtask == TL_PICK) {
+        v.force = P[(f0 + 6) * stride + r];
+        v.g = R.grasped[r] != 0;
+      } else if (c.subtask == TL_PLACE) {
+        v.tor = P[f0 * stride + r];
+        v.dist = P[(f0 + 5) * stride + r];
+        v.g = R.grasped[r] != 0;
+      } else {
+        v.tor = P[f0 * stride + r];
+        v.force = P[(f0 + 6) * stride + r];
+        v.art = P[(f0 + 8) * stride + r];
+      }
+      record_bits(c, v, sc_ru, sc_d, ind, err);
+      if (step_success) step_success[r] = (err & ERR_SUCC) ? 2 : ((ind & IND_SUCCESS) ? 1 : 0);
+    }
+    uint32_t prev = __shfl_up_sync(kFull, ind, 1);
+    if (lane == 0) prev = S.prev_ind;
+    const uint32_t mask = (valid && t > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
+    if (valid && step_mask) step_mask[r] = (uint8_t)mask;
+    lstate_fold(S, mask, valid ? err : 0u);
+    S.prev_ind = __shfl_sync(kFull, ind, 31);
+  }
+}
+
 // ---- K1: label_records -------------------------------------------------------
 constexpr int kLabelWarps = 8;
 
@@ -587,66 +675,13 @@ __global__ void __launch_bounds__(kLabelWarps * 32)
     if (c.subtask == TL_CLOSE && n > 0) close_cut(c, (double)P[(f0 + 8) * stride + rs], sc_ru, sc_d);
     // f32 episodes whose records are 16-byte aligned: 4 records per lane,
     // 128-bit loads (k_label_vec4); otherwise one record per lane below.
-    if (sizeof(T) == 4 && c.rest_zero && (rs & 3) == 0 && vec_ok) {
+    if (sizeof(T) == 4 && c.rest_zero && (rs & 3) == 0 && vec_ok &&
+        rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride) {
       label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
       if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
       continue;
     }
-    for (int t0 = 0; t0 < n; t0 += 32) {
-      const int t = t0 + lane;
-      const bool valid = t < n;
-      const int64_t r = rs + t;
-      RecV<T> v;
-      uint32_t ind = 0, err = 0;
-      if (valid) {
-        v.der = P[(f0 + 4) * stride + r];
-        v.cum = P[(f0 + 7) * stride + r];
-        v.vx = P[(f0 + 1) * stride + r];
-        v.vy = P[(f0 + 2) * stride + r];
-        v.om = P[(f0 + 3) * stride + r];
-        // Python-max of |q_i - rest_i| and of |qd_i|
-        T m = 0, mq = 0;
-        double md = 0.0;
-#pragma unroll
-        for (int i = 0; i < DOFMAX; i++) {
-          if (i < dof) {
-            const T q = P[i * stride + r];
-            const T qd = P[(dof + i) * stride + r];
-            const T aq = tabs(q), aqd = tabs(qd);
-            m = i == 0 ? aq : pymax_step(m, aq);
-            mq = i == 0 ? aqd : pymax_step(mq, aqd);
-            if (!c.rest_zero) {
-              const double dv = fabs(__dsub_rn((double)q, c.rest_arm[i]));
-              md = i == 0 ? dv : pymax_step(md, dv);
-            }
-          }
-        }
-        v.jm = m;
-        v.qdm = mq;
-        v.jm_d = md;
-        v.tor = 0; v.dist = 0; v.force = 0; v.art = 0; v.g = false;
-        if (c.subtask == TL_PICK) {
-          v.force = P[(f0 + 6) * stride + r];
-          v.g = R.grasped[r] != 0;
-        } else if (c.subtask == TL_PLACE) {
-          v.tor = P[f0 * stride + r];
-          v.dist = P[(f0 + 5) * stride + r];
-          v.g = R.grasped[r] != 0;
-        } else {
-          v.tor = P[f0 * stride + r];
-          v.force = P[(f0 + 6) * stride + r];
-          v.art = P[(f0 + 8) * stride + r];
-        }
-        record_bits(c, v, sc_ru, sc_d, ind, err);
-        if (step_success) step_success[r] = (err & ERR_SUCC) ? 2 : ((ind & IND_SUCCESS) ? 1 : 0);
-      }
-      uint32_t prev = __shfl_up_sync(kFull, ind, 1);
-      if (lane == 0) prev = S.prev_ind;
-      const uint32_t mask = (valid && t > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
-      if (valid && step_mask) step_mask[r] = (uint8_t)mask;
-      lstate_fold(S, mask, valid ? err : 0u);
-      S.prev_ind = __shfl_sync(kFull, ind, 31);
-    }
+    label_scalar<T, DOFMAX>(R, c, rs, n, sc_ru, sc_d, S, step_mask, step_success);
     if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
   }
 }

@@ -9,6 +9,7 @@
 
 #include "tl_common.cuh"
 #include "tl_label.cuh"
+#include "tl_label_tma.cuh"
 #include "tl_synth.cuh"
 #include "tl_synth_cta.cuh"
 #include "tl_filter.cuh"
@@ -177,7 +178,25 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
   const int grid = blocks_for(n_env, kLabelWarps, sm_count() * 16);
   const dim3 blk(kLabelWarps * 32);
   const bool small = recs->dof <= 7;
-  if (recs->dtype == 0) {
+  // TL_LABEL_TMA=1 selects the shared-memory (TMA bulk copy) staged variant;
+  // it is slower than the register path + L2 bulk prefetch at the occupancy
+  // its buffers allow (profiles/r1_ncu_summary.md), kept for A/B runs.
+  const bool use_tma = getenv("TL_LABEL_TMA") != nullptr;
+  if (recs->dtype == 0 && use_tma) {
+    if (small) {
+      using SM7 = LabelTmaSmem<7>;
+      set_max_smem(k_label_tma<7>, (int)sizeof(SM7));
+      k_label_tma<7><<<blocks_for(n_env, SM7::kWarps, sm_count()), SM7::kWarps * 32, sizeof(SM7),
+                       S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success,
+                                    labels);
+    } else {
+      using SM16 = LabelTmaSmem<16>;
+      set_max_smem(k_label_tma<16>, (int)sizeof(SM16));
+      k_label_tma<16><<<blocks_for(n_env, SM16::kWarps, sm_count()), SM16::kWarps * 32,
+                        sizeof(SM16), S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask,
+                                                   step_success, labels);
+    }
+  } else if (recs->dtype == 0) {
     if (small) k_label<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
     else k_label<float, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
   } else {

@@ -392,3 +392,22 @@ def test_fused_scan_emit_matches_two_pass(C, TH, kind):
     tot = int(a.ev_off[-1])
     assert torch.equal(a.ev_kind[:tot], b.ev_kind[:tot])
     assert torch.equal(a.ev_t[:tot], b.ev_t[:tot])
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_label_tma_variant_matches(C, TH, kind, monkeypatch):
+    """The shared-memory (TMA bulk copy) staged label kernel (TL_LABEL_TMA=1,
+    A/B variant) gives the same labels / masks / success bits as the fixtures."""
+    monkeypatch.setenv("TL_LABEL_TMA", "1")
+    c = fuzz_corpus(kind)
+    for align in (False, True):
+        rb, env, cs, n = corpus_batch(C, TH, c, align=align)
+        check_labels(C.label_records(rb, env, cs, n), c)
+    d = npz("crafted")
+    cc = Corpus(d, "f32_")
+    fields = list(d["threshold_fields"])
+    ov = [dict(zip(fields, map(float, d["f32_override"][i]))) if d["f32_has_override"][i] else None
+          for i in range(cc.n)]
+    rb, env, cs, n = corpus_batch(C, TH, cc, np.float32, ov, align=True)
+    res = C.label_records(rb, env, cs, n, want_success=True)
+    check_labels(res, cc, d["f32_err_type"])
