@@ -414,7 +414,7 @@ def main():
     all_seeds = (torch.arange(K + W, device=dev, dtype=torch.int64)[:, None] * world + rank) * N_ENV \
         + torch.arange(N_ENV, device=dev, dtype=torch.int64)[None, :]
     seeds_buf = torch.empty(N_ENV, dtype=torch.int64, device=dev)
-    ev_cap = N_ENV * cap
+    ev_cap = 4 * N_ENV * cap   # tl_fuzz_ev bound: <= 4 events per record
     ev_off = torch.empty(N_ENV + 1, dtype=torch.int64, device=dev)
     ev_kind = torch.empty(ev_cap, dtype=torch.uint8, device=dev)
     ev_t = torch.empty(ev_cap, dtype=torch.int32, device=dev)
@@ -427,22 +427,22 @@ def main():
     torch.cuda.set_stream(stream)
 
     def synth_only(s):
+        # reset kernel + realize kernel; the realize kernel also builds the
+        # ordered event lists (decoupled look-back over episodes)
         sp = ctypes.c_void_p(s.cuda_stream)
-        L.check(lib.tl_fuzz(L.ptr(seeds_buf), N_ENV, KIND, ctypes.byref(cfg_c), ctypes.byref(th_c),
-                            L.ptr(cs), None, ctypes.byref(rb_c), cap, None, None, None,
-                            L.ptr(ws.step_mask), L.ptr(ws.labels), L.ptr(ws.scratch), sp),
-                "tl_fuzz")
+        L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), N_ENV, KIND, ctypes.byref(cfg_c),
+                               ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
+                               None, None, None, L.ptr(ws.step_mask), L.ptr(ws.labels),
+                               L.ptr(ev_off), L.ptr(ev_kind), L.ptr(ev_t), ev_cap,
+                               L.ptr(ws.scratch), sp), "tl_fuzz_ev")
 
     def step_body(s):
         sp = ctypes.c_void_p(s.cuda_stream)
         synth_only(s)
-        L.check(lib.tl_scan_emit_events(L.ptr(ws.step_mask), L.ptr(ws.rec_start), L.ptr(ws.n_rec),
-                                        L.ptr(ws.labels), N_ENV, L.ptr(ev_off), L.ptr(ev_kind),
-                                        L.ptr(ev_t), L.ptr(scan_scratch), sp), "scan_emit")
         if world > 1:
             L.check(lib.tl_mode_histogram(L.ptr(ws.labels), N_ENV, L.ptr(hist), sp), "hist")
 
-    launches_per_step = 3 + (1 if world > 1 else 0)  # reset, realize, scan+emit
+    launches_per_step = 2 + (1 if world > 1 else 0)  # reset, realize(+events) [, histogram]
 
     # warm-up (also sets kernel attributes before graph capture)
     seeds_buf.copy_(all_seeds[0])
@@ -601,10 +601,10 @@ def main():
                    "parallelism": f"episodes sharded over {world} GPU(s), NCCL label all-gather",
                    "l2": "flushed between timed steps (256 MiB write, excluded from timing)",
                    "timing": "CUDA events per step on the launch stream, max over ranks",
-                   "step": "1 CUDA graph: tl_fuzz (reset + realize kernels) + tl_scan_emit_events"
+                   "step": "1 CUDA graph: tl_fuzz_ev (reset kernel + realize kernel that also emits the ordered event lists)"
                            + (" + tl_mode_histogram, then NCCL all_gather/all_reduce" if world > 1 else "")},
         "gpu_launches": launches_per_step * K,
-        "roofline": {"kernel": "k_synth (tl_fuzz)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": "k_fuzz_reset + k_synth_cta (tl_fuzz_ev)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,

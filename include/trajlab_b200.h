@@ -250,6 +250,19 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask,
             tl_script* scripts, uint8_t* step_mask, tl_label* labels,
             void* scratch, void* stream);
 
+/* tl_fuzz + the ordered event lists in the same launch pair: ev_off[n+1],
+ * (ev_kind, ev_t) at ev_off[e] as tl_scan_emit_events would produce them
+ * (a decoupled look-back over episodes inside the realize kernel).
+ * step_mask is required; ev_capacity >= 4 * n_env * cap_per_env. */
+int tl_fuzz_ev(const int64_t* seeds, int32_t n_env, int32_t subtask,
+               const tl_fuzz_cfg* cfg /* host */,
+               const tl_thresholds* th_realize /* host */,
+               const tl_cset* label_csets, const tl_rules* rules /* host */,
+               tl_records* out, int32_t cap_per_env, uint8_t* script_kind,
+               int32_t* script_gap, tl_script* scripts, uint8_t* step_mask,
+               tl_label* labels, int64_t* ev_off, uint8_t* ev_kind, int32_t* ev_t,
+               int64_t ev_capacity, void* scratch, void* stream);
+
 /* realize given scripts (device array) then label; out->rec_start/n_rec
  * are INPUTS here (host computed the layout).  label_csets indexed
  * [subtask*3 + articulation kind]; episodes may mix subtasks.

@@ -148,6 +148,9 @@ def lib():
         "tl_fuzz_scratch_bytes": ([i32, P(FuzzCfg_c)], ctypes.c_size_t),
         "tl_fuzz": ([vp, i32, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
                      P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "tl_fuzz_ev": ([vp, i32, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
+                        P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
+                       ctypes.c_int),
         "tl_realize_scratch_bytes": ([i32], ctypes.c_size_t),
         "tl_realize": ([vp, vp, vp, i32, P(Thresholds_c), vp, vp, P(Records_c),
                         vp, vp, vp, vp], ctypes.c_int),
@@ -190,7 +193,7 @@ def exported_symbols():
             "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes",
             "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
             "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions",
-            "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets"]
+            "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets", "tl_fuzz_ev"]
 
 
 def check(rc, what):

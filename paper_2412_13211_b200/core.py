@@ -339,8 +339,10 @@ class SynthWorkspace:
 
 def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
                ws: Optional[SynthWorkspace] = None, want_scripts=False,
-               rules=None) -> SynthBatch:
-    """tl_fuzz: fuzz(seed) -> records + labels for every seed (one launch)."""
+               rules=None, events=False) -> SynthBatch:
+    """tl_fuzz: fuzz(seed) -> records + labels for every seed (one launch).
+    events=True: tl_fuzz_ev, the ordered event lists built inside the same
+    launch (SynthBatch.label_result holds ev_off / ev_kind / ev_t)."""
     torch = _torch()
     dev = L.device()
     if not torch.is_tensor(seeds):
@@ -354,20 +356,32 @@ def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
     c_cfg = L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0,
                         float(cfg.edge_density), float(cfg.success_prob))
     rc_rules = rules_c(rules)
-    rc = L.lib().tl_fuzz(L.ptr(seeds), n, int(subtask), ctypes.byref(c_cfg),
-                         ctypes.byref(thresholds_c(th_realize)), L.ptr(label_csets),
-                         ctypes.byref(rc_rules) if rc_rules is not None else None,
-                         ctypes.byref(rb.c()), cap,
-                         L.ptr(ws.script_kind) if want_scripts else None,
-                         L.ptr(ws.script_gap) if want_scripts else None,
-                         L.ptr(ws.scripts) if want_scripts else None,
-                         L.ptr(ws.step_mask), L.ptr(ws.labels), L.ptr(ws.scratch),
-                         L.stream_ptr())
-    L.check(rc, "tl_fuzz")
+    args = [L.ptr(seeds), n, int(subtask), ctypes.byref(c_cfg),
+            ctypes.byref(thresholds_c(th_realize)), L.ptr(label_csets),
+            ctypes.byref(rc_rules) if rc_rules is not None else None,
+            ctypes.byref(rb.c()), cap,
+            L.ptr(ws.script_kind) if want_scripts else None,
+            L.ptr(ws.script_gap) if want_scripts else None,
+            L.ptr(ws.scripts) if want_scripts else None,
+            L.ptr(ws.step_mask), L.ptr(ws.labels)]
+    res = None
+    if events:
+        ev_cap = 4 * n * cap
+        ev_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        ev_kind = torch.empty(ev_cap, dtype=torch.uint8, device=dev)
+        ev_t = torch.empty(ev_cap, dtype=torch.int32, device=dev)
+        rc = L.lib().tl_fuzz_ev(*args, L.ptr(ev_off), L.ptr(ev_kind), L.ptr(ev_t), ev_cap,
+                                L.ptr(ws.scratch), L.stream_ptr())
+        L.check(rc, "tl_fuzz_ev")
+        res = LabelResult(ws.labels, ws.step_mask, None)
+        res.ev_off, res.ev_kind, res.ev_t = ev_off, ev_kind, ev_t
+    else:
+        rc = L.lib().tl_fuzz(*args, L.ptr(ws.scratch), L.stream_ptr())
+        L.check(rc, "tl_fuzz")
     return SynthBatch(rb, ws.labels, ws.step_mask,
                       ws.scripts if want_scripts else None,
                       ws.script_kind if want_scripts else None,
-                      ws.script_gap if want_scripts else None)
+                      ws.script_gap if want_scripts else None, res)
 
 
 def realize_batch(scripts_np, step_kind, step_gap, th_realize: Thresholds, label_csets,

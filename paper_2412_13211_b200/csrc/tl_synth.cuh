@@ -77,6 +77,11 @@ struct SynthParams {
   tl_records out;
   uint8_t* step_mask;
   tl_label* labels;
+  // optional fused event lists (k_synth_cta): ordered (kind, t) at ev_off[e]
+  int64_t* ev_off;
+  uint8_t* ev_kind;
+  int32_t* ev_t;
+  unsigned long long* ev_state;  // [n_env] look-back status, zeroed per launch
 };
 
 __device__ __forceinline__ bool in_alpha(int k, int ev) {

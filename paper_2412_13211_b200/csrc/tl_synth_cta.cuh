@@ -107,6 +107,79 @@ __device__ __forceinline__ int block_max(int v, int32_t* red) {
   return m;
 }
 
+// ---- fused event lists ---------------------------------------------------------
+// Episode e publishes its event count as soon as its label is final
+// (aggregate flag); after its episode loop each CTA resolves the exclusive
+// prefix of its episodes by a warp-wide decoupled look-back over the
+// predecessors' statuses (aggregate or inclusive prefix), publishes the
+// inclusive prefix and writes the ordered (kind, t) list from the step
+// masks it wrote -- events.py:109-191 without a separate scan kernel.
+// Waits only ever target lower episode indices whose aggregates are
+// published without waiting, so the look-back cannot deadlock.
+__device__ __forceinline__ void ev_publish_agg(const SynthParams& p, int e, int n_ev) {
+  atomicExch(&p.ev_state[e], kTileAgg | (unsigned long long)n_ev);
+}
+
+__device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
+  const int lane = lane_id();
+  volatile unsigned long long* st = p.ev_state;
+  int64_t prefix = 0;
+  int j = e - 1;
+  while (j >= 0) {
+    const int idx = j - lane;
+    const unsigned long long v = idx >= 0 ? st[idx] : kTilePrefix;
+    const unsigned long long flag = v & ~kTileValMask;
+    const unsigned pm = __ballot_sync(kFull, flag == kTilePrefix);
+    const unsigned zm = __ballot_sync(kFull, flag == 0);
+    const int lim = pm ? __ffs(pm) - 1 : 31;             // lanes 0..lim are needed
+    const unsigned need = lim == 31 ? kFull : ((2u << lim) - 1u);
+    if (zm & need) continue;                              // a predecessor is not published yet
+    int64_t c = lane <= lim ? (int64_t)(v & kTileValMask) : 0;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+    prefix += c;
+    if (pm) break;
+    j -= 32;
+  }
+  return prefix;
+}
+
+template <int DOFMAX>
+__device__ void ev_emit_all(const SynthParams& p) {
+  const int lane = lane_id();
+  for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
+    const tl_label L = p.labels[e];
+    const int n_ev = L.n_events;
+    const int64_t prefix = ev_lookback(p, e);
+    if (lane == 0) {
+      atomicExch(&p.ev_state[e], kTilePrefix | (unsigned long long)(prefix + n_ev));
+      p.ev_off[e] = prefix;
+      if (e == p.n_env - 1) p.ev_off[p.n_env] = prefix + n_ev;
+    }
+    if (n_ev == 0) continue;
+    const int sub = L.subtask;
+    const int64_t rs = p.out.rec_start[e];
+    const int n = p.out.n_rec[e];
+    int64_t base = prefix;
+    for (int t0 = 0; t0 < n; t0 += 32) {
+      const int t = t0 + lane;
+      const uint32_t mask = t < n ? p.step_mask[rs + t] : 0u;
+      const int cnt = __popc(mask);
+      const int incl = warp_incl_scan(cnt);
+      int64_t pos = base + incl - cnt;
+      uint32_t m = mask;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        p.ev_kind[pos] = kAlpha[sub][k];
+        p.ev_t[pos] = t;
+        pos++;
+      }
+      base += __shfl_sync(kFull, incl, 31);
+    }
+  }
+}
+
 template <bool FUZZ, int DOFMAX>
 __global__ void __launch_bounds__(kCtaThreads, 7)
     k_synth_cta(SynthParams p) {
@@ -138,6 +211,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;
+        if (p.ev_off) ev_publish_agg(p, e, 0);
       }
       __syncthreads();
       continue;
@@ -155,6 +229,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;
         if (FUZZ) p.out.n_rec[e] = 0;
+        if (p.ev_off) ev_publish_agg(p, e, 0);
       }
     };
     if (st0 != TL_OK) {
@@ -491,12 +566,17 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
     if (err_code) {
       fail(err_code, err_step);
     } else if (warp == 0) {
-      finish_label(c, LS, d0, p.rules, &p.labels[e]);
+      const tl_label L = make_label(c, LS, d0, p.rules);
+      if (lane == 0) {
+        p.labels[e] = L;
+        if (p.ev_off) ev_publish_agg(p, e, L.n_events);
+      }
     }
     __syncthreads();
     if (tid == 0 && e == 0) TL_STAMP(13);
     if (tid == 0 && e == gridDim.x) TL_STAMP(14);
   }
+  if (p.ev_off && warp == 0) ev_emit_all<DOFMAX>(p);
 }
 
 }  // namespace tl

@@ -302,18 +302,19 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
   const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
   return align256(n * kMtN * 4) + align256(n * sizeof(tl_script)) + align256(n * ms) +
-         align256(n * ms * 4);
+         align256(n * ms * 4) + align256(n * 8);  // + event look-back states (tl_fuzz_ev)
 }
 
 size_t tl_realize_scratch_bytes(int32_t n_env) {
   return align256((size_t)(n_env > 0 ? n_env : 1) * kMtN * 4);
 }
 
-int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
-            const tl_thresholds* th_realize, const tl_cset* label_csets, const tl_rules* rules,
-            tl_records* out, int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
-            tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* scratch,
-            void* stream) {
+static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
+                     const tl_thresholds* th_realize, const tl_cset* label_csets,
+                     const tl_rules* rules, tl_records* out, int32_t cap_per_env,
+                     uint8_t* script_kind, int32_t* script_gap, tl_script* scripts,
+                     uint8_t* step_mask, tl_label* labels, int64_t* ev_off, uint8_t* ev_kind,
+                     int32_t* ev_t, void* scratch, void* stream) {
   if (!cfg || !th_realize || !label_csets || !out || !labels || !scratch || n_env < 0 ||
       subtask < 0 || subtask > 3 || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
       cfg->max_gap < 1 || cfg->max_tail < 1 || cfg->max_events < 0 ||
@@ -332,6 +333,8 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_
   sp.step_kind = script_kind ? script_kind : reinterpret_cast<uint8_t*>(base);
   base += align256(n * ms);
   sp.step_gap = script_gap ? script_gap : reinterpret_cast<int32_t*>(base);
+  base += align256(n * ms * 4);
+  sp.ev_state = reinterpret_cast<unsigned long long*>(base);
   sp.seeds = seeds;
   sp.fuzz_subtask = subtask;
   sp.cfg = *cfg;
@@ -343,7 +346,38 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_
   sp.out = *out;
   sp.step_mask = step_mask;
   sp.labels = labels;
+  if (ev_off) {  // tl_fuzz_ev: fused ordered event lists
+    sp.ev_off = ev_off;
+    sp.ev_kind = ev_kind;
+    sp.ev_t = ev_t;
+    if (cudaMemsetAsync(sp.ev_state, 0, n * 8, S(stream))) return TL_E_CUDA;
+  }
   return launch_synth(sp, true, stream);
+}
+
+int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
+            const tl_thresholds* th_realize, const tl_cset* label_csets, const tl_rules* rules,
+            tl_records* out, int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
+            tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* scratch,
+            void* stream) {
+  return fuzz_impl(seeds, n_env, subtask, cfg, th_realize, label_csets, rules, out, cap_per_env,
+                   script_kind, script_gap, scripts, step_mask, labels, nullptr, nullptr, nullptr,
+                   scratch, stream);
+}
+
+int tl_fuzz_ev(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
+               const tl_thresholds* th_realize, const tl_cset* label_csets, const tl_rules* rules,
+               tl_records* out, int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
+               tl_script* scripts, uint8_t* step_mask, tl_label* labels, int64_t* ev_off,
+               uint8_t* ev_kind, int32_t* ev_t, int64_t ev_capacity, void* scratch,
+               void* stream) {
+  if (!ev_off || !ev_kind || !ev_t || !step_mask ||
+      ev_capacity < (int64_t)n_env * cap_per_env * 4)  // <= 4 events per record (Open/Close)
+    return TL_E_INVALID;
+  if (n_env == 0) return cudaMemsetAsync(ev_off, 0, 8, S(stream)) ? TL_E_CUDA : TL_OK;
+  return fuzz_impl(seeds, n_env, subtask, cfg, th_realize, label_csets, rules, out, cap_per_env,
+                   script_kind, script_gap, scripts, step_mask, labels, ev_off, ev_kind, ev_t,
+                   scratch, stream);
 }
 
 int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t* step_gap,

@@ -411,3 +411,27 @@ def test_label_tma_variant_matches(C, TH, kind, monkeypatch):
     rb, env, cs, n = corpus_batch(C, TH, cc, np.float32, ov, align=True)
     res = C.label_records(rb, env, cs, n, want_success=True)
     check_labels(res, cc, d["f32_err_type"])
+
+
+@pytest.mark.parametrize("kind", range(4))
+@pytest.mark.parametrize("n", [1, 37, 5000])
+def test_fused_synth_events_match_two_pass(C, TH, kind, n):
+    """tl_fuzz_ev (event lists built inside the realize kernel by a look-back
+    over episodes) == tl_fuzz + tl_scan_events + tl_emit_events."""
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_gap=64, max_tail=64)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    seeds = np.arange(n) + 4242
+    fused = C.fuzz_batch(seeds, kind, cfg, TH(), cs, events=True)
+    f_off = fused.label_result.ev_off.clone()
+    tot = int(f_off[-1])
+    f_kind = fused.label_result.ev_kind[:tot].clone()
+    f_t = fused.label_result.ev_t[:tot].clone()
+    f_lab = fused.labels.clone()
+    sb = C.fuzz_batch(seeds, kind, cfg, TH(), cs)
+    a = C.LabelResult(sb.labels, sb.step_mask, None)
+    C.emit_events(sb.records, a)
+    assert torch.equal(f_lab, sb.labels)
+    assert torch.equal(f_off, a.ev_off)
+    assert torch.equal(f_kind, a.ev_kind[:tot])
+    assert torch.equal(f_t, a.ev_t[:tot])
