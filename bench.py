@@ -437,10 +437,7 @@ def main():
                                L.ptr(ws.scratch), sp), "tl_fuzz_ev")
 
     def step_body(s):
-        sp = ctypes.c_void_p(s.cuda_stream)
         synth_only(s)
-        if world > 1:
-            L.check(lib.tl_mode_histogram(L.ptr(ws.labels), N_ENV, L.ptr(hist), sp), "hist")
 
     launches_per_step = 2 + (1 if world > 1 else 0)  # reset, realize(+events) [, histogram]
 
@@ -455,9 +452,14 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def collectives():
+        # the one exchange step: all-gather the 24-byte labels
+        # over NCCL; every rank then builds the global mode histogram from the
+        # gathered labels itself (no second collective)
         if world > 1:
             dist.all_gather_into_tensor(gathered.view(-1), ws.labels.view(-1))
-            dist.all_reduce(hist)
+            L.check(lib.tl_mode_histogram(L.ptr(gathered), world * N_ENV, L.ptr(hist),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                    "hist")
 
     for k in range(W):
         seeds_buf.copy_(all_seeds[K + k])
@@ -602,7 +604,7 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write, excluded from timing)",
                    "timing": "CUDA events per step on the launch stream, max over ranks",
                    "step": "1 CUDA graph: tl_fuzz_ev (reset kernel + realize kernel that also emits the ordered event lists)"
-                           + (" + tl_mode_histogram, then NCCL all_gather/all_reduce" if world > 1 else "")},
+                           + (", then NCCL all_gather of labels + tl_mode_histogram of the gathered labels" if world > 1 else "")},
         "gpu_launches": launches_per_step * K,
         "roofline": {"kernel": "k_fuzz_reset + k_synth_cta (tl_fuzz_ev)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,

@@ -77,7 +77,7 @@ class ShardResult:
 
 def fuzz_label_sharded(n_total: int, subtask: int, cfg, th=None, group=None, seed0=0):
     """Each rank fuzzes + labels its seed shard on its GPU (one fused launch
-    pair), then labels are all-gathered and the mode histogram all-reduced."""
+    pair), then labels are all-gathered; every rank histograms the gathered set."""
     import torch
     import torch.distributed as dist
     from . import core
@@ -91,12 +91,12 @@ def fuzz_label_sharded(n_total: int, subtask: int, cfg, th=None, group=None, see
     seeds = torch.arange(seed0 + lo, seed0 + hi, dtype=torch.int64, device=dev)
     cs = core.synth_csets(th).to_device(dev)
     sb = core.fuzz_batch(seeds, subtask, cfg, th, cs)
-    hist = core.mode_histogram(sb.labels, hi - lo)
     if world > 1:
         all_labels = allgather_labels(sb.labels[:hi - lo], group)
-        allreduce_hist(hist, group)
     else:
         all_labels = sb.labels[:hi - lo]
+    # global histogram from the gathered labels: no second collective
+    hist = core.mode_histogram(all_labels, int(all_labels.shape[0]))
     return ShardResult(sb.labels[:hi - lo], all_labels, hist, lo, hi)
 
 
