@@ -63,49 +63,82 @@ __device__ __forceinline__ uint32_t seed_step1(uint32_t prev, uint32_t tab, int 
 template <int KLEN>
 __device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t k1,
                                              uint32_t* out) {
-  uint32_t prev = kTlInitGenrand[0];
+  // The chain is 5 dependent integer ops per step; the table / old-word
+  // operands of group g+1 are loaded while group g runs (register double
+  // buffer), so no load latency lands on the chain.
+  const uint32_t* T = kTlInitGenrand;
+  uint32_t prev = T[0];
   // first loop, k = max(624, klen) = 624 iterations: i = 1..623, then i = 1
-  const uint32_t v1 = seed_step1<KLEN>(prev, kTlInitGenrand[1], 1, k0, k1);
+  const uint32_t v1 = seed_step1<KLEN>(prev, T[1], 1, k0, k1);
   mt[1] = v1;
   prev = v1;
-  int i0 = 2;
-  for (; i0 + 8 <= kMtN; i0 += 8) {
-    uint32_t tab[8];
+  uint32_t a[8], b[8];
 #pragma unroll
-    for (int k = 0; k < 8; k++) tab[k] = kTlInitGenrand[i0 + k];
+  for (int k = 0; k < 8; k++) a[k] = T[2 + k];
+  for (int g = 0; g < 76; g += 2) {  // groups i0 = 2 + 8g, g < 76 (2..609)
+    const int i0 = 2 + 8 * g;
+#pragma unroll
+    for (int k = 0; k < 8; k++) b[k] = T[i0 + 8 + k];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      prev = seed_step1<KLEN>(prev, tab[k], i0 + k, k0, k1);
+      prev = seed_step1<KLEN>(prev, a[k], i0 + k, k0, k1);
       mt[i0 + k] = prev;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = T[i0 + 16 + k];  // <= 617 + 8 < 624
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      prev = seed_step1<KLEN>(prev, b[k], i0 + 8 + k, k0, k1);
+      mt[i0 + 8 + k] = prev;
     }
   }
 #pragma unroll
-  for (int k = 0; k < (kMtN - 2) % 8; k++) {
-    prev = seed_step1<KLEN>(prev, kTlInitGenrand[i0 + k], i0 + k, k0, k1);
-    mt[i0 + k] = prev;
+  for (int k = 0; k < 8; k++) {  // group 76: 610..617
+    prev = seed_step1<KLEN>(prev, a[k], 610 + k, k0, k1);
+    mt[610 + k] = prev;
+  }
+#pragma unroll
+  for (int k = 0; k < 6; k++) {  // 618..623
+    prev = seed_step1<KLEN>(prev, T[618 + k], 618 + k, k0, k1);
+    mt[618 + k] = prev;
   }
   mt[0] = prev;
   prev = seed_step1<KLEN>(prev, v1, kMtN, k0, k1);  // 624th iteration: i = 1, j = 623 % klen
   mt[1] = prev;
   // second loop: N-1 iterations, i = 2..623 then wrap to i = 1
-  i0 = 2;
-  for (; i0 + 8 <= kMtN; i0 += 8) {
-    uint32_t old[8];
+  auto step2 = [](uint32_t pv, uint32_t old, int i) {
+    return (old ^ ((pv ^ (pv >> 30)) * 1566083941u)) - (uint32_t)i;
+  };
 #pragma unroll
-    for (int k = 0; k < 8; k++) old[k] = mt[i0 + k];
+  for (int k = 0; k < 8; k++) a[k] = mt[2 + k];
+  for (int g = 0; g < 76; g += 2) {
+    const int i0 = 2 + 8 * g;
+#pragma unroll
+    for (int k = 0; k < 8; k++) b[k] = mt[i0 + 8 + k];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      prev = (old[k] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i0 + k);
+      prev = step2(prev, a[k], i0 + k);
       out[i0 + k] = prev;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = mt[i0 + 16 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      prev = step2(prev, b[k], i0 + 8 + k);
+      out[i0 + 8 + k] = prev;
     }
   }
 #pragma unroll
-  for (int k = 0; k < (kMtN - 2) % 8; k++) {
-    prev = (mt[i0 + k] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i0 + k);
-    out[i0 + k] = prev;
+  for (int k = 0; k < 8; k++) {
+    prev = step2(prev, a[k], 610 + k);
+    out[610 + k] = prev;
   }
-  const uint32_t m1 = (mt[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
-  out[1] = m1;
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    prev = step2(prev, mt[618 + k], 618 + k);
+    out[618 + k] = prev;
+  }
+  out[1] = step2(prev, mt[1], 1);
   out[0] = 0x80000000u;
 }
 
