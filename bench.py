@@ -278,7 +278,9 @@ def env_api_run(dev, stream, n_env=4096, T=200, reps=10):
         res[name] = {"ms": 1e3 * t, "env_steps_per_s": records / t,
                      "achieved_GBps": records * 94.0 / t / 1e9, "frac_hbm": records * 94.0 / t / 1e9 / hbm}
     lab, nrec = env.labels()
-    assert (lab["status"] == 0).all() and int(nrec.sum()) == records
+    if not ((lab["status"] == 0).all() and int(nrec.sum()) == records):
+        raise RuntimeError(f"env rollout check failed: statuses {np.unique(lab['status'])}, "
+                           f"records {int(nrec.sum())} != {records}")
     res["note"] = ("records = env steps actually emitted (scripts end before T -> IDLE); "
                    "94 B/env-step written (93 B record + 1 B event mask)")
     return res

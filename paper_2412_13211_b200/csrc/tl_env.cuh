@@ -66,6 +66,10 @@ __host__ __device__ inline size_t env_bytes(int n) {
 
 struct EnvParams {
   EnvHdr* hdr;
+  // reset: header contents by value / source pointer (written into hdr by
+  // the reset kernel itself, so a captured CUDA graph replays them)
+  tl_thresholds th;
+  const tl_cset* src_cs;
   EnvSt* st;
   uint32_t* mt;
   int32_t n_env;
@@ -277,8 +281,8 @@ struct EnvSmem {
 };
 
 template <int DOFMAX>
-__device__ __forceinline__ void env_stage_csets(EnvSmem<DOFMAX>& sm, const EnvHdr* hdr) {
-  const uint32_t* s = reinterpret_cast<const uint32_t*>(hdr->cs);
+__device__ __forceinline__ void env_stage_csets(EnvSmem<DOFMAX>& sm, const tl_cset* cs) {
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(cs);
   uint32_t* d = reinterpret_cast<uint32_t*>(sm.cs);
   for (int i = threadIdx.x; i < (int)(sizeof(sm.cs) / 4); i += blockDim.x) d[i] = __ldg(s + i);
   __syncthreads();
@@ -291,7 +295,17 @@ template <int DOFMAX>
 __global__ void __launch_bounds__(kEnvThreads) k_env_reset(EnvParams p) {
   extern __shared__ __align__(16) unsigned char env_smem_raw[];
   EnvSmem<DOFMAX>& sm = *reinterpret_cast<EnvSmem<DOFMAX>*>(env_smem_raw);
-  env_stage_csets(sm, p.hdr);
+  env_stage_csets(sm, p.src_cs);
+  if (blockIdx.x == 0) {  // header for the step kernels
+    if (threadIdx.x == 0) {
+      p.hdr->th = p.th;
+      p.hdr->n_env = p.n_env;
+      p.hdr->dof = p.dof;
+    }
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(sm.cs);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(p.hdr->cs);
+    for (int i = threadIdx.x; i < (int)(sizeof(sm.cs) / 4); i += blockDim.x) dst[i] = src[i];
+  }
   const int e = blockIdx.x * kEnvThreads + threadIdx.x;
   if (e >= p.n_env) return;
   const tl_script sc = p.scripts[e];
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(kEnvThreads) k_env_reset(EnvParams p) {
   for (int k = 0; k < 7; k++) s.last[k] = -1;
   s.err_t = -1;
   RzConst z;
-  int code = sc.n_steps < 0 ? TL_ERR_SCRIPT_CAPACITY : env_rz(z, s, p.hdr->th, p.dof);
+  int code = sc.n_steps < 0 ? TL_ERR_SCRIPT_CAPACITY : env_rz(z, s, p.th, p.dof);
   if (!code && sc.subtask == TL_PICK && sc.initial_grasped && !sc.initial_contact)
     code = TL_INF_PICK_GRASPED_NO_CONTACT;                               // synth.py:154-155
   const bool art_ok = sc.art_kind >= 0 && sc.art_kind <= 2;

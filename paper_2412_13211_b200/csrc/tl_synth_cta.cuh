@@ -197,10 +197,13 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
   for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
     if (tid == 0 && e == 0) TL_STAMP(10);
     // ---------------- script + seeded RNG state -------------------------------
-    const tl_script sc = p.scripts[e];
-    const int64_t rs = p.out.rec_start[e];
-    const int n_rec = p.out.n_rec[e];
+    tl_script sc;
+    int64_t rs;
+    int n_rec;
     {
+      sc = p.scripts[e];
+      rs = p.out.rec_start[e];
+      n_rec = p.out.n_rec[e];
       const uint32_t* src = p.states + (int64_t)e * kMtN;
       for (int i = tid; i < kMtN; i += kCtaThreads) S.mt[i] = src[i];
     }

@@ -268,19 +268,7 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
 
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   const int rows_smem = 32 * kRowWords * 4;
-  if (fuzz) {
-    if (sp.n_env <= 32 * sm_count()) {  // latency-bound batch: one episode per warp
-      const int sm1 = 2 * kRowWords * 4;
-      k_fuzz_reset<1><<<sp.n_env, 32, sm1, S(stream)>>>(sp);
-    } else {
-      set_max_smem(k_fuzz_reset<16>, rows_smem);
-      k_fuzz_reset<16><<<(sp.n_env + 15) / 16, 32, rows_smem, S(stream)>>>(sp);
-    }
-  } else {
-    set_max_smem(k_seed_states, rows_smem);
-    k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
-  }
-  // realize + label: one 2-warp CTA per episode (tl_synth_cta.cuh)
+  // realize + label: one 3-warp CTA per episode (tl_synth_cta.cuh)
   const bool small = sp.out.dof <= 7;
   const int smem = small ? (int)sizeof(CtaSmem<7>) : (int)sizeof(CtaSmem<16>);
   void (*k)(SynthParams) = fuzz ? (small ? k_synth_cta<true, 7> : k_synth_cta<true, 16>)
@@ -289,6 +277,18 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCtaThreads, smem);
   if (per_sm < 1) per_sm = 1;
+  if (fuzz) {
+    if (sp.n_env <= 32 * sm_count()) {  // latency-bound batch: one episode per warp
+      const int sm1 = 2 * kRowWords * 4;
+      k_fuzz_reset<1><<<sp.n_env, 32, sm1, S(stream)>>>(sp);
+    } else {
+      set_max_smem(k_fuzz_reset<16>, rows_smem);
+      k_fuzz_reset<16><<<(sp.n_env + 15) / 16, 32, rows_smem, S(stream)>>>(sp);
+    }
+  } else if (!fuzz) {
+    set_max_smem(k_seed_states, rows_smem);
+    k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
+  }
   const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
   if (getenv("TL_DEBUG"))
     fprintf(stderr, "k_synth_cta: %d CTAs/SM (smem %d B, %d threads), grid %d\n", per_sm, smem,
@@ -419,19 +419,12 @@ static EnvParams env_params(void* state, int32_t n_env, int32_t dof) {
   return ep;
 }
 
-static int env_write_hdr(const EnvParams& ep, const tl_thresholds* th, const tl_cset* csets,
-                         int32_t n_env, int32_t dof, void* stream) {
-  // pageable source: cudaMemcpyAsync stages it before returning
-  EnvHdr h;
-  memset(&h, 0, sizeof(h));
-  h.th = *th;
-  h.n_env = n_env;
-  h.dof = dof;
-  if (cudaMemcpyAsync(&ep.hdr->th, &h.th, sizeof(h.th), cudaMemcpyHostToDevice, S(stream)) ||
-      cudaMemcpyAsync(&ep.hdr->n_env, &h.n_env, 16, cudaMemcpyHostToDevice, S(stream)) ||
-      cudaMemcpyAsync(ep.hdr->cs, csets, sizeof(h.cs), cudaMemcpyDeviceToDevice, S(stream)))
-    return TL_E_CUDA;
-  return TL_OK;
+// The header (realize thresholds, label csets, sizes) is written by the
+// reset kernel from its by-value parameters: no host-memory copy is captured
+// into CUDA graphs.
+static void env_set_hdr(EnvParams& ep, const tl_thresholds* th, const tl_cset* csets) {
+  ep.th = *th;
+  ep.src_cs = csets;
 }
 
 static int env_launch_reset(EnvParams& ep, void* stream) {
@@ -458,7 +451,7 @@ int tl_env_reset(void* state, int32_t n_env, int32_t dof, const tl_script* scrip
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
   EnvParams ep = env_params(state, n_env, dof);
-  if (int rc = env_write_hdr(ep, th_realize, label_csets, n_env, dof, stream)) return rc;
+  env_set_hdr(ep, th_realize, label_csets);
   SynthParams sp;
   memset(&sp, 0, sizeof(sp));
   sp.scripts = const_cast<tl_script*>(scripts);
@@ -488,7 +481,7 @@ int tl_env_reset_fuzz(void* state, const int64_t* seeds, int32_t n_env, int32_t 
   if (n_env == 0) return TL_OK;
   const int dof = 7;  // random_script builds arm_dof = 7 scripts (synth.py:63-74)
   EnvParams ep = env_params(state, n_env, dof);
-  if (int rc = env_write_hdr(ep, th_realize, label_csets, n_env, dof, stream)) return rc;
+  env_set_hdr(ep, th_realize, label_csets);
   SynthParams sp;
   memset(&sp, 0, sizeof(sp));
   sp.seeds = seeds;
