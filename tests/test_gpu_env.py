@@ -269,3 +269,34 @@ def test_env_idle_and_hold_semantics():
     la, _ = a.labels()
     lb, _ = b.labels()
     assert la.tobytes() == lb.tobytes()
+
+
+def test_env_cuda_graph_replay():
+    """reset + step captured in a CUDA graph replays to the same episodes
+    (the reset writes its header from kernel parameters, not host memory)."""
+    import paper_2412_13211_b200 as P
+    n, T = 512, 120
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        env = P.BatchedSubtaskEnv(n)
+        seeds = torch.arange(n, dtype=torch.int64, device="cuda") + 99
+        cfg = P.FuzzConfig(max_gap=32, max_tail=32)
+        b0 = env._outputs(1, None)
+        bT = env._outputs(T, None)
+        env.reset(seeds=seeds, subtask=P.SubtaskKind.Place, config=cfg, out=b0)
+        acts = env.scripted_actions(1, T)
+        env.step(acts, out=bT)
+        want_lab, want_n = env.labels()
+        want_obs = bT.obs.clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            env.reset(seeds=seeds, subtask=P.SubtaskKind.Place, config=cfg, out=b0)
+            env.step(acts, out=bT)
+        for _ in range(2):
+            bT.obs.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            lab, nrec = env.labels()
+            assert lab.tobytes() == want_lab.tobytes() and np.array_equal(nrec, want_n)
+            live = (acts != P.env.IDLE).unsqueeze(0).expand_as(bT.obs)
+            assert torch.equal(bT.obs.view(torch.int32)[live], want_obs.view(torch.int32)[live])
