@@ -148,8 +148,8 @@ template <int DOFMAX>
 __device__ void ev_emit_all(const SynthParams& p) {
   const int lane = lane_id();
   for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
-    const tl_label L = p.labels[e];
-    const int n_ev = L.n_events;
+    // this episode's own aggregate (the labels may live in host memory)
+    const int n_ev = (int)(((volatile unsigned long long*)p.ev_state)[e] & kTileValMask);
     const int64_t prefix = ev_lookback(p, e);
     if (lane == 0) {
       atomicExch(&p.ev_state[e], kTilePrefix | (unsigned long long)(prefix + n_ev));
@@ -157,7 +157,7 @@ __device__ void ev_emit_all(const SynthParams& p) {
       if (e == p.n_env - 1) p.ev_off[p.n_env] = prefix + n_ev;
     }
     if (n_ev == 0) continue;
-    const int sub = L.subtask;
+    const int sub = p.fuzz_subtask;  // fused event lists are a fuzz (single-subtask) path
     const int64_t rs = p.out.rec_start[e];
     const int n = p.out.n_rec[e];
     int64_t base = prefix;

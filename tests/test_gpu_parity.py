@@ -435,3 +435,36 @@ def test_fused_synth_events_match_two_pass(C, TH, kind, n):
     assert torch.equal(f_off, a.ev_off)
     assert torch.equal(f_kind, a.ev_kind[:tot])
     assert torch.equal(f_t, a.ev_t[:tot])
+
+
+def test_fused_events_zero_copy_host_outputs(C, TH):
+    """tl_fuzz_ev writing labels and event lists straight into pinned host
+    memory (the e2e path) == the device-memory outputs."""
+    import ctypes
+    from paper_2412_13211_b200 import _lib as L
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_gap=64, max_tail=64)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 1024
+    seeds = torch.arange(n, dtype=torch.int64, device="cuda") + 555
+    ref = C.fuzz_batch(seeds, 1, cfg, TH(), cs, events=True)
+    tot = int(ref.label_result.ev_off[-1])
+    cap = C.fuzz_capacity(cfg)
+    ws = C.SynthWorkspace(n, cap)
+    ev_cap = 4 * n * cap
+    h_lab = torch.empty((n, 24), dtype=torch.uint8).pin_memory()
+    h_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+    h_k = torch.empty(ev_cap, dtype=torch.uint8).pin_memory()
+    h_t = torch.empty(ev_cap, dtype=torch.int32).pin_memory()
+    rb = ws.records()
+    rc = L.lib().tl_fuzz_ev(L.ptr(seeds), n, 1, ctypes.byref(C.fuzz_cfg_c(cfg)),
+                            ctypes.byref(C.thresholds_c(TH())), L.ptr(cs), None,
+                            ctypes.byref(rb.c()), cap, None, None, None, L.ptr(ws.step_mask),
+                            L.ptr(h_lab), L.ptr(h_off), L.ptr(h_k), L.ptr(h_t), ev_cap,
+                            L.ptr(ws.scratch), L.stream_ptr())
+    L.check(rc, "tl_fuzz_ev")
+    torch.cuda.synchronize()
+    assert torch.equal(h_lab, ref.labels[:n].cpu())
+    assert torch.equal(h_off, ref.label_result.ev_off.cpu())
+    assert torch.equal(h_k[:tot], ref.label_result.ev_kind[:tot].cpu())
+    assert torch.equal(h_t[:tot], ref.label_result.ev_t[:tot].cpu())
