@@ -84,6 +84,23 @@ class NoiseModel:
     seed: int = 0
 
 
+def sample_noise(model: NoiseModel, arm_dof: int = 7, rng=None):
+    """(arm perturbation [arm_dof], base (x, y), base rotation) from clipped
+    Gaussians (synth.py:43-54).  Host-side: it draws from a CPython
+    random.Random (gauss() keeps its own cached second normal), is not on
+    the realize/fuzz path, and is only mirrored for API completeness."""
+    import random as _random
+    r = rng if rng is not None else _random.Random(model.seed)
+
+    def draw(std, lim):
+        v = r.gauss(0.0, std)
+        return min(lim, v) if v > -lim else -lim
+
+    arm = tuple(draw(model.arm_std, model.arm_clip) for _ in range(arm_dof))
+    base = (draw(model.base_std, model.base_clip), draw(model.base_std, model.base_clip))
+    return arm, base, draw(model.rot_std, model.rot_clip)
+
+
 def _label_csets(th_label=None, dof=7):
     key = (th_label or Thresholds()).astuple() + (dof,)
     cache = _label_csets.__dict__.setdefault("cache", {})
