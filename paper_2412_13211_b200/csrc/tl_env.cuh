@@ -364,29 +364,29 @@ __global__ void __launch_bounds__(kEnvThreads) k_env_reset(EnvParams p) {
 }
 
 // step: k_steps records per env (actions[k][e]): _advance_cum, _apply, _emit.
-// Four lanes (a quad) share one env: the plan is computed redundantly by
-// the quad, the MT window copies, the draws and the plane stores are split
-// four ways (draw d -> lane d % 4: the pre-draws of cum / dist are draws 0..pre-1,
-// plane k is draw pre + k), and lane 0 gathers the record for the label fold.
-constexpr int kQuad = 4;
-constexpr int kEnvQThreads = 128;             // 32 envs per block
-constexpr int kEnvQPerBlock = kEnvQThreads / kQuad;
+// LPE lanes (4 or 8) share one env: the plan is computed redundantly by the
+// group, the MT window copies, the draws and the plane stores are split LPE
+// ways (draw d -> lane d % LPE: the pre-draws of cum / dist are draws
+// 0..pre-1, plane k is draw pre + k), and lane 0 gathers the record for the
+// label fold.
+constexpr int kEnvQThreads = 128;             // 128 / LPE envs per block
 
-template <int DOFMAX>
+template <int DOFMAX, int LPE>
 struct EnvQSmem {
+  static constexpr int kEnvs = kEnvQThreads / LPE;
   static constexpr int kWords = 2 * (2 + 2 * DOFMAX + 5);  // max words per step
   static constexpr int kBuf = 2 * kWords + 1;              // old[kWords+1] + src[kWords]
   static constexpr int kStride = 2 * kBuf + 1;             // two buffers per env; odd
   tl_cset cs[12];
-  uint32_t buf[kEnvQPerBlock * kStride];
+  uint32_t buf[kEnvs * kStride];
 };
 
-// lane q of the quad copies words j = q, q+4, ... of the window
-template <int MAXW>
+// lane q of the env's lane group copies words j = q, q+LPE, ... of the window
+template <int MAXW, int LPE>
 __device__ __forceinline__ void env_stage_async_q(const uint32_t* __restrict__ mt, int idx,
                                                   uint32_t* so, uint32_t* ss, int q) {
 #pragma unroll
-  for (int j0 = 0; j0 <= MAXW; j0 += kQuad) {
+  for (int j0 = 0; j0 <= MAXW; j0 += LPE) {
     const int j = j0 + q;
     if (j <= MAXW) {
       int i = idx + j;
@@ -395,7 +395,7 @@ __device__ __forceinline__ void env_stage_async_q(const uint32_t* __restrict__ m
     }
   }
 #pragma unroll
-  for (int j0 = 0; j0 < MAXW; j0 += kQuad) {
+  for (int j0 = 0; j0 < MAXW; j0 += LPE) {
     const int j = j0 + q;
     if (j < MAXW) {
       int i = idx + j + kMtM;
@@ -407,9 +407,10 @@ __device__ __forceinline__ void env_stage_async_q(const uint32_t* __restrict__ m
   cp_async_commit();
 }
 
-template <int DOFMAX>
+template <int DOFMAX, int LPE>
 __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
-  using SM = EnvQSmem<DOFMAX>;
+  using SM = EnvQSmem<DOFMAX, LPE>;
+  constexpr int kQuad = LPE;  // lanes per env (4 or 8)
   extern __shared__ __align__(16) unsigned char env_smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(env_smem_raw);
   {
@@ -420,9 +421,9 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
   }
   const int q = threadIdx.x & (kQuad - 1);
   const int le = threadIdx.x / kQuad;
-  const int e = blockIdx.x * kEnvQPerBlock + le;
+  const int e = blockIdx.x * SM::kEnvs + le;
   const int qbase = lane_id() & ~(kQuad - 1);
-  const unsigned qmask = 0xFu << qbase;
+  const unsigned qmask = ((1u << kQuad) - 1u) << qbase;
   if (e >= p.n_env) return;  // whole quads leave together
   EnvSt s;
   env_load(s, &p.st[e]);
@@ -441,10 +442,12 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
   const int64_t st = p.obs_stride;
   const float fnan = __int_as_float(0x7fc00000);
   int cur = 0;  // buffer holding the window at s.mt_idx
-  env_stage_async_q<SM::kWords>(mt, s.mt_idx, row, row + SM::kWords + 1, q);
+  env_stage_async_q<SM::kWords, LPE>(mt, s.mt_idx, row, row + SM::kWords + 1, q);
   int a_next = p.actions[e];
   for (int k = 0; k < p.k_steps; k++) {
     const int64_t col = (int64_t)k * n + e;
+    const bool stamp = e == 0 && q == 0 && k == 5;  // profiling build only
+    if (stamp) TL_STAMP(100);
     const int a = a_next;
     if (k + 1 < p.k_steps) a_next = p.actions[col + n];  // prefetch
     if (a == TL_ACT_IDLE || s.status) {
@@ -494,6 +497,7 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
       s.at_rest = (uint8_t)ps.at_rest;
       s.level = (uint8_t)ps.level;
     }
+    if (stamp) TL_STAMP(101);
     const bool emit = !s.at_rest;
     const int pre = adv + app;
     const int nw = 2 * (pre + (emit ? ne : 0));
@@ -504,17 +508,24 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
     const uint32_t* ss = so + SM::kWords + 1;
     {  // next step's window into the other buffer; this one complete quad-wide
       uint32_t* no = row + (cur ^ 1) * SM::kBuf;
-      env_stage_async_q<SM::kWords>(mt, s.mt_idx, no, no + SM::kWords + 1, q);
+      env_stage_async_q<SM::kWords, LPE>(mt, s.mt_idx, no, no + SM::kWords + 1, q);
       cp_async_wait<1>();
       __syncwarp(qmask);
       cur ^= 1;
     }
+    if (stamp) TL_STAMP(102);
     // this lane's draws: d = q, q + 4, ... over pre-draws then planes
     double r_pre = 0.0;
     float mq = 0.f, mqd = 0.f, sc5[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
     double md = 0.0;
     const int nd = pre + ne;
-    for (int d = q; d < nd; d += kQuad) {
+    // unrolled to the compile-time maximum so the independent draws of a
+    // lane interleave (the loop-carried form serialised ~470 cycles each)
+    constexpr int kMaxIt = (2 + 2 * DOFMAX + 5 + kQuad - 1) / kQuad;
+#pragma unroll
+    for (int it = 0; it < kMaxIt; it++) {
+      const int d = q + it * kQuad;
+      if (d >= nd) continue;
       const bool draw = d < pre || emit;
       const double r = draw ? env_rand(mt, idx, 2 * d, so, ss) : 0.0;
       if (d < pre) {
@@ -546,6 +557,7 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
         sc5[4] = j == 4 ? v : sc5[4];
       }
     }
+    if (stamp) TL_STAMP(103);
     // cum / dist from the pre-draws (lanes 0 and adv), identical on all lanes
     if (adv) {
       const double rc = __shfl_sync(qmask, r_pre, qbase);
@@ -561,22 +573,26 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
     const float vforce = z.has_force ? __double2float_rn(s.force) : fnan;
     const float vcum = __double2float_rn(s.cum);
     const float vart = z.has_art ? __double2float_rn(s.art) : fnan;
-    {
+    if (q < 4) {
       const int f = 2 * dof + 5 + q;  // dist, force, cum, art: one plane per lane
       p.obs[(int64_t)f * st + col] = q == 0 ? vdist : q == 1 ? vforce : q == 2 ? vcum : vart;
     }
+    if (stamp) TL_STAMP(104);
     // gather the record's predicate inputs on lane 0
-    mq = fmaxf(mq, __shfl_xor_sync(qmask, mq, 1));
-    mq = fmaxf(mq, __shfl_xor_sync(qmask, mq, 2));
-    mqd = fmaxf(mqd, __shfl_xor_sync(qmask, mqd, 1));
-    mqd = fmaxf(mqd, __shfl_xor_sync(qmask, mqd, 2));
+#pragma unroll
+    for (int x = 1; x < kQuad; x <<= 1) {
+      mq = fmaxf(mq, __shfl_xor_sync(qmask, mq, x));
+      mqd = fmaxf(mqd, __shfl_xor_sync(qmask, mqd, x));
+    }
     if (!c.rest_zero) {
-      md = fmax(md, __shfl_xor_sync(qmask, md, 1));
-      md = fmax(md, __shfl_xor_sync(qmask, md, 2));
+#pragma unroll
+      for (int x = 1; x < kQuad; x <<= 1) md = fmax(md, __shfl_xor_sync(qmask, md, x));
     }
     float sv[5];
 #pragma unroll
-    for (int j = 0; j < 5; j++) sv[j] = __shfl_sync(qmask, sc5[j], qbase + ((pre + 2 * dof + j) & 3));
+    for (int j = 0; j < 5; j++)
+      sv[j] = __shfl_sync(qmask, sc5[j], qbase + ((pre + 2 * dof + j) & (kQuad - 1)));
+    if (stamp) TL_STAMP(105);
     if (q == 0) {
       if (p.obs_grasped) p.obs_grasped[col] = s.grasped;
       RecV<float> v;
@@ -591,6 +607,7 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
       s.prev_ind = ind;
       if (p.step_mask) p.step_mask[col] = (uint8_t)m;
     }
+    if (stamp) TL_STAMP(106);
   }
   cp_async_wait<0>();
   if (q == 0) env_store(&p.st[e], s);

@@ -522,13 +522,20 @@ int tl_env_step(void* state, int32_t n_env, int32_t dof, const uint8_t* actions,
   ep.obs_stride = obs_stride;
   ep.obs_grasped = obs_grasped;
   ep.step_mask = step_mask;
-  const int grid = (n_env + kEnvQPerBlock - 1) / kEnvQPerBlock;
+  // 8 lanes per env while the batch leaves SMs idle (latency-bound), 4 when
+  // it fills the GPU (less redundant per-env planning); 16 measured slower
+  const bool wide = (int64_t)n_env * 8 <= (int64_t)sm_count() * 1024;
+  auto go = [&](auto kern, int lpe, size_t smem) {
+    set_max_smem(kern, (int)smem);
+    const int per_block = kEnvQThreads / lpe;
+    kern<<<(n_env + per_block - 1) / per_block, kEnvQThreads, smem, S(stream)>>>(ep);
+  };
   if (dof <= 7) {
-    set_max_smem(k_env_step<7>, (int)sizeof(EnvQSmem<7>));
-    k_env_step<7><<<grid, kEnvQThreads, sizeof(EnvQSmem<7>), S(stream)>>>(ep);
+    if (wide) go(k_env_step<7, 8>, 8, sizeof(EnvQSmem<7, 8>));
+    else go(k_env_step<7, 4>, 4, sizeof(EnvQSmem<7, 4>));
   } else {
-    set_max_smem(k_env_step<16>, (int)sizeof(EnvQSmem<16>));
-    k_env_step<16><<<grid, kEnvQThreads, sizeof(EnvQSmem<16>), S(stream)>>>(ep);
+    if (wide) go(k_env_step<16, 8>, 8, sizeof(EnvQSmem<16, 8>));
+    else go(k_env_step<16, 4>, 4, sizeof(EnvQSmem<16, 4>));
   }
   return check_launch();
 }
