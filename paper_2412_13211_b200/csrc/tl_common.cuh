@@ -151,55 +151,6 @@ __device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed, uint32_t* 
   else mt_seed_impl<1>(mt, k0, 0u, out);
 }
 
-// Warp-cooperative regeneration of all 624 words in place (CPython's
-// genrand "generate N words at one time"); tempered outputs also go to
-// ring[(ring_base + i) & ring_mask].  Word i reads mt[i], mt[i+1] (old) and
-// mt[i+397] (old, i < 227) or mt[i-227] (new, i >= 227), so a group of up
-// to 7 consecutive 32-word iterations can load before any of them stores.
-template <int IT>
-__device__ __forceinline__ int twist_src(int i) {
-  return IT < 7 ? i + kMtM : IT > 7 ? i - (kMtN - kMtM) : (i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM));
-}
-
-template <int IT0, int NG>
-__device__ __forceinline__ void twist_group(uint32_t* mt, uint32_t* ring, uint32_t base,
-                                            uint32_t mask, int lane) {
-  uint32_t nv[NG];
-#pragma unroll
-  for (int g = 0; g < NG; g++) {
-    const int i = (IT0 + g) * 32 + lane;
-    nv[g] = mt_mix(mt[i], mt[i + 1], mt[g == 0 ? twist_src<IT0>(i) : g == 1 ? twist_src<IT0 + 1>(i)
-                                          : g == 2 ? twist_src<IT0 + 2>(i) : twist_src<IT0 + 3>(i)]);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int g = 0; g < NG; g++) {
-    const int i = (IT0 + g) * 32 + lane;
-    mt[i] = nv[g];
-    ring[(base + (uint32_t)i) & mask] = mt_temper(nv[g]);
-  }
-}
-
-__device__ __forceinline__ void mt_twist_warp(uint32_t* mt, uint32_t* ring,
-                                              uint32_t ring_base, uint32_t ring_mask) {
-  const int lane = lane_id();
-  twist_group<0, 4>(mt, ring, ring_base, ring_mask, lane);
-  twist_group<4, 4>(mt, ring, ring_base, ring_mask, lane);
-  twist_group<8, 4>(mt, ring, ring_base, ring_mask, lane);
-  twist_group<12, 4>(mt, ring, ring_base, ring_mask, lane);
-  twist_group<16, 3>(mt, ring, ring_base, ring_mask, lane);
-  // words 608..623 (word 623 wraps to the new mt[0])
-  uint32_t nv = 0;
-  const int i = 608 + lane;
-  if (lane < 16) nv = mt_mix(mt[i], mt[lane == 15 ? 0 : i + 1], mt[i - (kMtN - kMtM)]);
-  __syncwarp();
-  if (lane < 16) {
-    mt[i] = nv;
-    ring[(ring_base + (uint32_t)i) & ring_mask] = mt_temper(nv);
-  }
-  __syncwarp();
-}
-
 // Serial reader over a freshly seeded MT state for one thread (script
 // sampling).  Words are regenerated lazily in order, in place: word i of a
 // block reads mt[i+1] (old) and mt[i+397] (old) or mt[i-227] (already new),

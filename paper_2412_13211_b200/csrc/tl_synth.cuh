@@ -1,5 +1,7 @@
-// tl_synth.cuh -- batched env reset/step: random_script + realize, fused
-// with online labelling (one warp per episode).
+// tl_synth.cuh -- random_script + realize building blocks: the reset
+// kernels (CPython seeding, script sampling), the realizer constants and
+// the deterministic part of _apply; the realize + label kernel itself is
+// k_synth_cta (tl_synth_cta.cuh), the batched env in tl_env.cuh.
 //
 // Reference (paths under /root/reference/pkg/src/trajlab/):
 //   synth.py:100-162  _Realizer.__init__  (= reset)
@@ -11,43 +13,24 @@
 // Every record t >= 1 is one env step: advance_cum (1 draw before the
 // ExcessiveCollisions jump), apply (1 draw for ObjAtGoal/ObjLeftGoal) and
 // emit (2*dof+5 draws unless at rest).  Which draws happen depends only on
-// the script, not on drawn values, so a per-step plan (lane 0, O(steps))
-// fixes the MT word offset of every record; the 32 lanes of the warp then
-// generate 32 records at once from a shared ring of tempered MT words.
-// Only cum_robot_force is a true serial f64 recurrence (lane 0, 4 ops per
-// record).  Object distance draws and their feasibility checks happen at
-// the owning event record.
+// the script, not on drawn values, so a per-step plan (one thread,
+// O(steps)) fixes the MT word offset of every record and the records of a
+// wave are generated in parallel from a ring of tempered MT words.  Only
+// cum_robot_force is a true serial f64 recurrence (4 ops per record).
+// Object distance draws and their feasibility checks happen at the owning
+// event record.
 #pragma once
 #include "tl_label.cuh"
 
 namespace tl {
 
-constexpr int kRingWords = 2048;  // >= 32 records * 42 words + 623
-constexpr uint32_t kRingMask = kRingWords - 1;
 constexpr int kMaxSteps = 64;     // script steps planned per window
-constexpr int kSynthWarps = 4;
 
 struct StepSt {          // realizer state after a step (index s+1); [0] = before
   float force, art;      // record values (f32)
   uint8_t grasped, at_rest, exc, level;
   int16_t last_draw;     // window-local step of the latest dist draw, -1 = carry
   int16_t pad;
-};
-
-struct SynthWarp {
-  uint32_t mt[kMtN];            // realize RNG state
-  uint32_t ring[kRingWords];    // tempered words; [0, 624) = script RNG state first
-  int32_t gap[kMaxSteps];
-  int32_t tau[kMaxSteps];       // record index of step s's event
-  int32_t W[kMaxSteps + 1];     // word offset of segment s's first record
-  int32_t hw[kMaxSteps + 1];    // words per hold record in segment s
-  StepSt st[kMaxSteps + 1];
-  double dist_after[kMaxSteps];
-  double radv[32];
-  uint8_t kind[kMaxSteps];
-  uint8_t sflag[kMaxSteps];     // bit0 dist draw at the event
-  int32_t misc[16];
-  tl_cset cs;                   // labelling constants (staged)
 };
 
 struct RzConst {
@@ -435,328 +418,6 @@ __global__ void __launch_bounds__(32) k_seed_states(SynthParams p) {
   const int64_t e0 = (int64_t)blockIdx.x * 32;
   const int64_t e = e0 + lane;
   if (e < p.n_env) mt_seed_lane(rows + lane * kRowWords, p.scripts[e].seed, p.states + e * kMtN);
-}
-
-template <bool FUZZ, int DOFMAX>
-__global__ void __launch_bounds__(kSynthWarps * 32)
-    k_synth(SynthParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  SynthWarp& S = reinterpret_cast<SynthWarp*>(smem_raw)[warp];
-  const int dof = p.out.dof;
-  float* __restrict__ P = reinterpret_cast<float*>(p.out.planes);
-  const int64_t stride = p.out.plane_stride;
-  const float fnan = __int_as_float(0x7fc00000);
-
-  for (int e = blockIdx.x * kSynthWarps + warp; e < p.n_env; e += gridDim.x * kSynthWarps) {
-    // ---------------- script + seeded RNG state from the reset kernel --------
-    const tl_script sc = p.scripts[e];
-    const int64_t rs = p.out.rec_start[e];
-    const int n_rec = p.out.n_rec[e];
-    {
-      const uint32_t* src = p.states + (int64_t)e * kMtN;
-      for (int i = lane; i < kMtN; i += 32) S.mt[i] = src[i];
-    }
-    if (FUZZ && sc.n_steps < 0) {
-      if (lane == 0) {
-        tl_label L;
-        L.status = TL_ERR_SCRIPT_CAPACITY; L.n_events = 0; L.err_index = -1;
-        L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
-        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
-        p.labels[e] = L;
-      }
-      continue;
-    }
-    __syncwarp();
-    const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
-    stage_cset(&S.cs, &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
-    RzConst z;
-    int st0 = realizer_init(z, sc, p.th, dof);
-    auto fail = [&](int code, int step) {
-      if (lane == 0) {
-        tl_label L;
-        L.status = code; L.n_events = 0; L.err_index = step;
-        L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
-        L.d0 = __longlong_as_double(0x7ff8000000000000ll);
-        p.labels[e] = L;
-        if (FUZZ) p.out.n_rec[e] = 0;
-      }
-    };
-    if (st0 != TL_OK) { fail(st0, -1); continue; }
-
-    // initial realizer state (synth.py:111-158)
-    PlanSt ps;
-    ps.force = (z.has_force && sc.initial_contact) ? 1.2 : 0.0;
-    ps.grasped = sc.initial_grasped ? 1 : 0;
-    ps.at_rest = 0;
-    ps.exc = 0;
-    if (z.kind == TL_OPEN) {
-      ps.level = sc.initial_level;
-      ps.art = sc.initial_level == TL_LVL_LOW ? z.lv_low : sc.initial_level == TL_LVL_SLIGHT ? z.lv_slight : z.lv_open;
-    } else if (z.kind == TL_CLOSE) {
-      ps.level = sc.initial_level == TL_LVL_CLOSED ? TL_LVL_CLOSED : TL_LVL_OPEN;
-      ps.art = z.a_q0;
-    } else {
-      ps.level = TL_LVL_LOW;
-      ps.art = 0.0;
-    }
-    const double dist0 = z.has_goal ? sc.initial_dist_obj_goal : __longlong_as_double(0x7ff8000000000000ll);
-    const tl_cset& c = S.cs;
-    float sc_ru = 0.f;
-    double sc_d = 0.0;
-    if (c.subtask == TL_CLOSE) close_cut(c, (double)__double2float_rn(ps.art), sc_ru, sc_d);
-    const double d0 = (double)__double2float_rn(dist0);
-
-    // --------------- step windows -------------------------------------------
-    LState LS;
-    lstate_init(LS);
-    double cum = 0.0;            // warp-uniform serial f64 recurrence
-    double dist_carry = dist0;   // dist before the window
-    int32_t w_carry = 2 * z.ne;  // record 0 emits 2*dof+5 draws
-    int32_t tau_prev = 0;
-    uint32_t produced = 0;
-    int err_code = 0, err_step = -1;
-    int s_base = 0;
-    const int n_steps = sc.n_steps;
-    PlanSt pcarry = ps;
-    bool first_window = true;
-    for (;;) {
-      const int ns = min(n_steps - s_base, kMaxSteps);
-      const bool last_window = s_base + ns >= n_steps;
-      for (int i = lane; i < ns; i += 32) {
-        S.kind[i] = p.step_kind[sc.step_off + s_base + i];
-        S.gap[i] = p.step_gap[sc.step_off + s_base + i];
-      }
-      __syncwarp();
-      // ---- plan (lane 0): record/word layout + deterministic state ------------
-      if (lane == 0) {
-        PlanSt q = pcarry;
-        int32_t w = w_carry, r = tau_prev;
-        int last_draw = -1, perr = 0, pstep = ns;
-        S.st[0] = make_st(z, q, -1);
-        for (int s = 0; s < ns; s++) {
-          const int g = S.gap[s];
-          if (g < 1) { perr = TL_INF_GAP; pstep = s; S.W[s] = w; S.hw[s] = 0; S.tau[s] = r; break; }
-          S.W[s] = w;
-          const int hwv = (q.exc ? 0 : 2) + (q.at_rest ? 0 : 2 * z.ne);
-          S.hw[s] = hwv;
-          w += (g - 1) * hwv;
-          r += g;
-          S.tau[s] = r;
-          int wev = q.exc ? 0 : 2;
-          int draw = 0;
-          const int ec = plan_apply(z, q, S.kind[s], draw);
-          S.sflag[s] = (uint8_t)draw;
-          if (ec) { perr = ec; pstep = s; break; }
-          if (draw) last_draw = s;
-          wev += (draw ? 2 : 0) + (q.at_rest ? 0 : 2 * z.ne);
-          w += wev;
-          S.st[s + 1] = make_st(z, q, last_draw);
-        }
-        if (!perr) {
-          S.W[ns] = w;
-          S.hw[ns] = (q.exc ? 0 : 2) + (q.at_rest ? 0 : 2 * z.ne);
-        }
-        S.misc[0] = perr;
-        S.misc[1] = pstep;
-        S.misc[2] = w;
-        S.misc[3] = r;
-        // carry for the next window
-        S.misc[4] = q.grasped; S.misc[5] = q.at_rest; S.misc[6] = q.exc; S.misc[7] = q.level;
-        reinterpret_cast<double*>(&S.misc[8])[0] = q.force;
-        reinterpret_cast<double*>(&S.misc[10])[0] = q.art;
-      }
-      __syncwarp();
-      const int perr = S.misc[0], pstep = S.misc[1];
-      // records of this window: (tau_prev, last event] or up to n_rec
-      const int r_begin = first_window ? 0 : tau_prev + 1;
-      int r_end;
-      if (perr) r_end = S.tau[pstep] + 1;
-      else if (last_window) r_end = n_rec;
-      else r_end = S.misc[3] + 1;
-      // ---- chunks of 32 records -----------------------------------------------
-      int seg_hint = 0;
-      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += 32) {
-        const int r = r0 + lane;
-        const bool valid = r < r_end;
-        int o = 0, adv = 0, app = 0, emit = 0, sidx = 0, ev = -1, s = 0;
-        if (valid) {
-          if (r == 0) {
-            emit = 1;  // initial record: no advance/apply, at_rest = False
-          } else {
-            s = seg_hint;
-            while (s < ns && S.tau[s] < r) s++;
-            if (s < ns && S.tau[s] == r) {
-              o = S.W[s] + (S.gap[s] - 1) * S.hw[s];
-              adv = !S.st[s].exc;
-              ev = S.kind[s];
-              app = (s < pstep || !perr) ? (S.sflag[s] & 1) : 0;
-              emit = (perr && s == pstep) ? 0 : !S.st[s + 1].at_rest;
-              sidx = (perr && s == pstep) ? s : s + 1;
-            } else {
-              const int first = (s == 0 ? tau_prev : S.tau[s - 1]) + 1;
-              o = S.W[s] + (r - first) * S.hw[s];
-              adv = !S.st[s].exc;
-              emit = !S.st[s].at_rest;
-              sidx = s;
-            }
-          }
-        }
-        seg_hint = __shfl_sync(kFull, s, 0);
-        // words needed by this chunk
-        const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
-        const int need_max = __reduce_max_sync(kFull, need);
-        while ((int)produced < need_max) {
-          mt_twist_warp(S.mt, S.ring, produced, kRingMask);
-          produced += kMtN;
-        }
-        const uint2* ring2 = reinterpret_cast<const uint2*>(S.ring);
-        auto rnd = [&](int woff) {
-          const uint2 wv = ring2[((uint32_t)woff & kRingMask) >> 1];
-          return rand53(wv.x, wv.y);
-        };
-        // advance_cum draw, object-distance draw and its feasibility check
-        int my_err = 0;
-        double my_radv = 0.0;
-        if (valid) {
-          if (adv) my_radv = rnd(o);
-          if (app) {
-            const double rr = rnd(o + 2 * adv);
-            S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rr) : uniform_rn(0.3, 0.8, rr);
-          }
-        }
-        __syncwarp();
-        double dist_rec = dist_carry;
-        if (valid && z.has_goal) {
-          const int ld = S.st[sidx].last_draw;
-          dist_rec = ld >= 0 ? S.dist_after[ld] : dist_carry;
-          if (ev >= 0) {
-            const int ldb = S.st[s].last_draw;
-            const double db = ldb >= 0 ? S.dist_after[ldb] : dist_carry;
-            switch (ev) {  // value-dependent checks of _apply (synth.py:218-260)
-              case TL_EV_OBJ_AT_GOAL: if (db <= z.goal) my_err = TL_INF_AT_GOAL_ALREADY; break;
-              case TL_EV_OBJ_LEFT_GOAL: if (db > z.goal) my_err = TL_INF_LEFT_NOT_AT_GOAL; break;
-              case TL_EV_RELEASED_AT_GOAL: if (db > z.goal) my_err = TL_INF_RAG; break;
-              case TL_EV_RELEASED_OUTSIDE_GOAL: if (db <= z.goal) my_err = TL_INF_ROG; break;
-              case TL_EV_SUCCESS: if (db > z.goal) my_err = TL_INF_SUCCESS_UNREACHABLE; break;
-            }
-          }
-        }
-        if (valid && perr && ev >= 0 && s == pstep && !my_err) my_err = perr;
-        const unsigned eb = __ballot_sync(kFull, my_err != 0);
-        if (eb) {
-          const int L = __ffs(eb) - 1;
-          err_code = __shfl_sync(kFull, my_err, L);
-          err_step = s_base + __shfl_sync(kFull, s, L);
-          break;
-        }
-        // cum_robot_force: the one serial f64 recurrence (synth.py:192-196,
-        // :210-213), run in lockstep by all lanes on shuffled draws (cum is
-        // warp-uniform).  uniform(0.0, b) = RN(b * r) exactly for b, r >= 0.
-        const int cnt = min(32, r_end - r0);
-        const bool my_exc = valid && ev == TL_EV_EXCESSIVE_COLLISIONS && !(perr && s == pstep);
-        // draw (or -1: no draw, or -2: jump to 1.05*limit) broadcast via smem
-        S.radv[lane] = my_exc ? -2.0 : (valid && adv ? my_radv : -1.0);
-        __syncwarp();
-        double my_cum = 0.0;
-#pragma unroll 4
-        for (int j = 0; j < cnt; j++) {
-          const double rj = S.radv[j];
-          const double nxt = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rj));
-          cum = rj >= 0.0 ? nxt : (rj < -1.5 ? z.L105 : cum);
-          my_cum = lane == j ? cum : my_cum;
-        }
-        const float my_cum32 = __double2float_rn(my_cum);
-        __syncwarp();
-        // ---- emit + write + label ---------------------------------------------
-        RecV<float> v;
-        uint32_t ind = 0, errb = 0;
-        if (valid) {
-          const int64_t rr = rs + r;
-          const StepSt stv = S.st[sidx];
-          const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
-          float* __restrict__ dst = P + rr;  // plane f at dst + f*stride
-          // emitted draws in source order (synth.py:178-185); at rest: zeros
-          auto draw = [&](uint32_t k, double a, double b) -> float {
-            if (!emit) return 0.f;
-            const uint2 wv = ring2[((eo + 2u * k) & kRingMask) >> 1];
-            return __double2float_rn(uniform_rn(a, b, rand53(wv.x, wv.y)));
-          };
-          float mq = 0.f, mqd = 0.f;
-#pragma unroll
-          for (int i = 0; i < DOFMAX; i++) {
-            if (i < dof) {
-              const float q = draw(i, -0.3, 0.3);
-              *dst = q;
-              dst += stride;
-              mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < DOFMAX; i++) {
-            if (i < dof) {
-              const float qd = draw(dof + i, -0.4, 0.4);
-              *dst = qd;
-              dst += stride;
-              mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
-            }
-          }
-          const uint32_t k2 = 2 * dof;
-          v.tor = draw(k2, -0.05, 0.05);
-          v.vx = draw(k2 + 1, -0.2, 0.2);
-          v.vy = draw(k2 + 2, -0.2, 0.2);
-          v.om = draw(k2 + 3, -0.3, 0.3);
-          v.der = draw(k2 + 4, 0.2, 1.0);
-          v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
-          v.force = stv.force;
-          v.cum = my_cum32;
-          v.art = stv.art;
-          v.g = stv.grasped != 0;
-          v.qdm = mqd;
-          v.jm = mq;
-          v.jm_d = 0.0;
-          dst[0] = v.tor;
-          dst[stride] = v.vx;
-          dst[2 * stride] = v.vy;
-          dst[3 * stride] = v.om;
-          dst[4 * stride] = v.der;
-          dst[5 * stride] = v.dist;
-          dst[6 * stride] = v.force;
-          dst[7 * stride] = v.cum;
-          dst[8 * stride] = v.art;
-          p.out.grasped[rr] = (uint8_t)v.g;
-          record_bits(c, v, sc_ru, sc_d, ind, errb);
-        }
-        uint32_t prev = __shfl_up_sync(kFull, ind, 1);
-        if (lane == 0) prev = LS.prev_ind;
-        const uint32_t mask = (valid && r > 0) ? edge_mask(c.subtask, prev, ind) : 0u;
-        if (valid && p.step_mask) p.step_mask[rs + r] = (uint8_t)mask;
-        lstate_fold(LS, mask, valid ? errb : 0u);
-        const int lastl = cnt - 1;
-        LS.prev_ind = __shfl_sync(kFull, ind, lastl);
-      }
-      // a plan error whose step has no event record of its own (gap < 1)
-      if (!err_code && perr) { err_code = perr; err_step = s_base + pstep; }
-      if (err_code || last_window) break;
-      // object distance carried into the next window
-      {
-        const int ld = S.st[ns].last_draw;
-        if (ld >= 0) dist_carry = S.dist_after[ld];
-      }
-      // next window
-      pcarry.grasped = S.misc[4]; pcarry.at_rest = S.misc[5]; pcarry.exc = S.misc[6]; pcarry.level = S.misc[7];
-      pcarry.force = reinterpret_cast<const double*>(&S.misc[8])[0];
-      pcarry.art = reinterpret_cast<const double*>(&S.misc[10])[0];
-      w_carry = S.misc[2];
-      tau_prev = S.misc[3];
-      s_base += ns;
-      first_window = false;
-      __syncwarp();
-    }
-    if (err_code) { fail(err_code, err_step); continue; }
-    finish_label(c, LS, d0, p.rules, &p.labels[e]);
-    __syncwarp();
-  }
 }
 
 }  // namespace tl
