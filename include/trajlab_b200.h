@@ -386,6 +386,16 @@ int tl_group_mode_counts(const tl_label* labels, const int32_t* group, int64_t n
 int tl_chain_progress(const tl_label* labels, const int64_t* slot_label, int64_t n_chain,
                       int32_t n_slots, int64_t* alive, void* stream);
 
+/* ---- the exchange step of the multi-GPU path --------------
+ * nccl_comm is the caller's ncclComm_t (one rank per GPU).  Equal-size
+ * shards: gathered[r*n_per_rank + i] = rank r's local[i] (pad the last shard).
+ * counts is summed in place over ranks (mode histograms, tl_group_mode_counts
+ * tables, progressive-completion alive counts).  NCCL is resolved from the
+ * process at call time (the library is not linked against it). */
+int tl_allgather_labels(void* nccl_comm, const tl_label* local, int64_t n_per_rank,
+                        tl_label* gathered, void* stream);
+int tl_allreduce_counts(void* nccl_comm, int64_t* counts, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

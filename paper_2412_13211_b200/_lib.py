@@ -173,6 +173,8 @@ def lib():
         "tl_group_mode_counts": ([vp, vp, i64, i32, vp, vp], ctypes.c_int),
         "tl_chain_progress": ([vp, vp, i64, i32, vp, vp], ctypes.c_int),
         "tl_filter_buckets": ([vp, vp, i64, vp, vp, vp, i32, vp, vp], ctypes.c_int),
+        "tl_allgather_labels": ([vp, vp, i64, vp, vp], ctypes.c_int),
+        "tl_allreduce_counts": ([vp, vp, i64, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -193,7 +195,8 @@ def exported_symbols():
             "tl_compact_records", "tl_fuzz_scratch_bytes", "tl_realize_scratch_bytes",
             "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
             "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions",
-            "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets", "tl_fuzz_ev"]
+            "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets", "tl_fuzz_ev",
+            "tl_allgather_labels", "tl_allreduce_counts"]
 
 
 def check(rc, what):

@@ -1,6 +1,8 @@
 // trajlab_b200.cu -- C ABI of libtrajlab_b200.so (see include/trajlab_b200.h).
 // Single translation unit: kernels live in the tl_*.cuh headers.
 #include <algorithm>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -83,6 +85,28 @@ int blocks_for(int n_items, int per_block, int max_blocks) {
 }
 
 }  // namespace
+
+// ---- the one exchange step over NCCL helpers ------------------
+// NCCL is resolved at call time from the process (the library that created
+// the caller's communicator, e.g. torch's bundled copy), never linked, so
+// libtrajlab_b200.so loads without NCCL and cannot pull in a second copy.
+namespace {
+using AllGatherFn = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                                     cudaStream_t);
+using AllReduceFn = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                     ncclComm_t, cudaStream_t);
+template <class F>
+F nccl_sym(const char* name) {
+  void* f = dlsym(RTLD_DEFAULT, name);
+  if (!f) {
+    static void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // an already-loaded NCCL
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) f = dlsym(h, name);
+  }
+  return reinterpret_cast<F>(f);
+}
+}  // namespace
+
 
 extern "C" {
 
@@ -600,6 +624,26 @@ int tl_filter_buckets(const tl_label* labels, const int32_t* key, int64_t n,
   k_filter_buckets<<<grid, 256, 0, S(stream)>>>(labels, key, n, rule_lut, pool, pool_b0, n_keys,
                                                bucket);
   return check_launch();
+}
+
+// ---- the one exchange step over NCCL ----------------------------
+int tl_allgather_labels(void* nccl_comm, const tl_label* local, int64_t n_per_rank,
+                        tl_label* gathered, void* stream) {
+  if (!nccl_comm || !local || !gathered || n_per_rank < 0) return TL_E_INVALID;
+  static AllGatherFn f = nccl_sym<AllGatherFn>("ncclAllGather");
+  if (!f) return TL_E_CUDA;
+  const ncclResult_t r = f(local, gathered, (size_t)n_per_rank * sizeof(tl_label), ncclUint8,
+                           reinterpret_cast<ncclComm_t>(nccl_comm), S(stream));
+  return r == ncclSuccess ? TL_OK : TL_E_CUDA;
+}
+
+int tl_allreduce_counts(void* nccl_comm, int64_t* counts, int64_t n, void* stream) {
+  if (!nccl_comm || !counts || n < 0) return TL_E_INVALID;
+  static AllReduceFn f = nccl_sym<AllReduceFn>("ncclAllReduce");
+  if (!f) return TL_E_CUDA;
+  const ncclResult_t r = f(counts, counts, (size_t)n, ncclInt64, ncclSum,
+                           reinterpret_cast<ncclComm_t>(nccl_comm), S(stream));
+  return r == ncclSuccess ? TL_OK : TL_E_CUDA;
 }
 
 size_t tl_filter_scratch_bytes(int64_t n, int32_t n_buckets, int32_t n_pools) {

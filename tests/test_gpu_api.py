@@ -305,3 +305,41 @@ def test_c5_device_filter_matches_host_filter():
     assert got_ids == [e.episode_id for e in want.entries]
     assert man.counts == want.counts
     assert man.shortfalls == want.shortfalls
+
+
+def test_nccl_exchange_entry_points_single_rank():
+    """tl_allgather_labels / tl_allreduce_counts through a 1-rank NCCL
+    communicator made with the process's NCCL (torch's bundled copy): the
+    C-ABI plumbing of the multi-GPU exchange step (symbol resolution, byte
+    counts, dtypes, stream)."""
+    import ctypes
+    import glob
+    import os
+    import numpy as np
+    import torch
+    from paper_2412_13211_b200 import _lib as L
+    base = os.path.dirname(torch.__file__)
+    paths = glob.glob(os.path.join(base, "..", "nvidia", "nccl", "lib", "libnccl.so*"))
+    nccl = ctypes.CDLL(paths[0] if paths else "libnccl.so.2", mode=ctypes.RTLD_GLOBAL)
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_char * 128)]
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    torch.cuda.set_device(0)
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    try:
+        n = 777
+        lab = torch.randint(0, 255, (n, 24), dtype=torch.uint8, device="cuda")
+        out = torch.zeros_like(lab)
+        L.check(L.lib().tl_allgather_labels(comm, L.ptr(lab), n, L.ptr(out), L.stream_ptr()),
+                "allgather")
+        counts = torch.arange(42 * 3, dtype=torch.int64, device="cuda")
+        want = counts.clone()
+        L.check(L.lib().tl_allreduce_counts(comm, L.ptr(counts), counts.numel(), L.stream_ptr()),
+                "allreduce")
+        torch.cuda.synchronize()
+        assert torch.equal(out, lab) and torch.equal(counts, want)
+    finally:
+        nccl.ncclCommDestroy(comm)
