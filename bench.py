@@ -327,6 +327,48 @@ def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
             "timing": "CUDA events around the whole pipeline (incl. host glue), max over ranks"}
 
 
+def c3_run(dev, stream, world, n_env=4096, reps=10):
+    """C3: Open and Close (fridge / drawer 50/50 via choice,
+    synth.py:374-376), 4096 envs per GPU each, fuzz(seed, kind) for seeds
+    [r*4096, (r+1)*4096), default FuzzConfig; generation + labels + event
+    lists (tl_fuzz_ev), device-timed per batch, max over ranks."""
+    import torch
+    import paper_2412_13211_b200 as P
+    from paper_2412_13211_b200 import core
+    rank = torch.distributed.get_rank() if world > 1 else 0
+    cfg = P.FuzzConfig()
+    cs = core.synth_csets(P.Thresholds()).to_device(dev)
+    seeds = torch.arange(rank * n_env, (rank + 1) * n_env, dtype=torch.int64, device=dev)
+    out = {}
+    for name, kind in (("open", 2), ("close", 3)):
+        ms, recs = [], 0
+        for k in range(reps + 2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sb = core.fuzz_batch(seeds, kind, cfg, P.Thresholds(), cs, events=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if k >= 2:
+                ms.append(a.elapsed_time(b))
+                recs = int(sb.records.n_rec.sum())
+        t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = float(t.item()) / 1e3
+        lab = sb.labels.cpu().numpy().reshape(-1).view(L_LABEL_DTYPE())
+        out[name] = {"ms": 1e3 * t, "env_steps_per_s": recs * world / t,
+                     "labelled_trajectories_per_s": n_env * world / t,
+                     "mean_steps": recs / n_env, "failed": int((lab["status"] != 0).sum())}
+    out["workload"] = ("C3: fuzz(seed, Open|Close), 4096 envs/GPU each, default FuzzConfig, "
+                       "generation + labels + ordered event lists (tl_fuzz_ev)")
+    return out
+
+
+def L_LABEL_DTYPE():
+    from paper_2412_13211_b200 import _lib
+    return _lib.LABEL_DTYPE
+
+
 def c4_run(dev, stream, world, n_chain=4096, reps=3):
     """C4: SetTable chains, 4096 per GPU; chain c runs Open,
     Pick, Place, Close twice with seeds 8c + k (k = 0..7); slot success =
@@ -591,6 +633,7 @@ def main():
         # ---- sizing run: k_label over 2^19 x 200-step episodes
         sizing = label_sizing_run(L, core, lib, dev, stream, flush)
         env_api = env_api_run(dev, stream)
+        c3 = c3_run(dev, stream, world)
         c5 = c5_run(dev, stream, world)
         c4 = c4_run(dev, stream, world)
     clk = clocks.summary()
@@ -656,6 +699,7 @@ def main():
                                          "generated record (93 B/env-step)"}},
         "label_sizing": sizing,
         "env_api": env_api,
+        "c3": c3,
         "c5": c5,
         "c4": c4,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",

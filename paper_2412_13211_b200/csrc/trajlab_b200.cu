@@ -290,6 +290,36 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
   return check_launch();
 }
 
+// k_fuzz_reset with EPW episodes per warp (2*EPW seeding lanes): one
+// episode per warp while that keeps <= 8 warps per SM, else 8 per warp --
+// the seeding chains are latency-bound and more warps contend for issue,
+// while the sampler is branchy code that diverges across episodes
+// (measured: scripts/reset_epw_ab.sh, 1k-250k episodes)
+static void launch_fuzz_reset(SynthParams& sp, void* stream) {
+  const int n = sp.n_env, sms = sm_count();
+  const char* force = getenv("TL_RESET_EPW");  // A/B measurement only
+  const int epw = force ? atoi(force) : ((int64_t)n <= (int64_t)sms * 8 ? 1 : 8);
+  const int smem = 2 * epw * kRowWords * 4;
+  switch (epw) {
+    case 1: k_fuzz_reset<1><<<n, 32, smem, S(stream)>>>(sp); break;
+    case 2:
+      set_max_smem(k_fuzz_reset<2>, smem);
+      k_fuzz_reset<2><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
+      break;
+    case 4:
+      set_max_smem(k_fuzz_reset<4>, smem);
+      k_fuzz_reset<4><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
+      break;
+    case 8:
+      set_max_smem(k_fuzz_reset<8>, smem);
+      k_fuzz_reset<8><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
+      break;
+    default:
+      set_max_smem(k_fuzz_reset<16>, 2 * 16 * kRowWords * 4);
+      k_fuzz_reset<16><<<(n + 15) / 16, 32, 2 * 16 * kRowWords * 4, S(stream)>>>(sp);
+  }
+}
+
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   const int rows_smem = 32 * kRowWords * 4;
   // realize + label: one 3-warp CTA per episode (tl_synth_cta.cuh)
@@ -302,13 +332,7 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCtaThreads, smem);
   if (per_sm < 1) per_sm = 1;
   if (fuzz) {
-    if (sp.n_env <= 32 * sm_count()) {  // latency-bound batch: one episode per warp
-      const int sm1 = 2 * kRowWords * 4;
-      k_fuzz_reset<1><<<sp.n_env, 32, sm1, S(stream)>>>(sp);
-    } else {
-      set_max_smem(k_fuzz_reset<16>, rows_smem);
-      k_fuzz_reset<16><<<(sp.n_env + 15) / 16, 32, rows_smem, S(stream)>>>(sp);
-    }
+    launch_fuzz_reset(sp, stream);
   } else if (!fuzz) {
     set_max_smem(k_seed_states, rows_smem);
     k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
@@ -322,6 +346,7 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
 
 size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
   const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
@@ -517,13 +542,7 @@ int tl_env_reset_fuzz(void* state, const int64_t* seeds, int32_t n_env, int32_t 
   sp.states = ep.mt;
   sp.n_env = n_env;
   sp.cap_per_env = 0x7fffffff;
-  const int rows_smem = 32 * kRowWords * 4;
-  if (n_env <= 32 * sm_count()) {
-    k_fuzz_reset<1><<<n_env, 32, 2 * kRowWords * 4, S(stream)>>>(sp);
-  } else {
-    set_max_smem(k_fuzz_reset<16>, rows_smem);
-    k_fuzz_reset<16><<<(n_env + 15) / 16, 32, rows_smem, S(stream)>>>(sp);
-  }
+  launch_fuzz_reset(sp, stream);
   ep.scripts = scripts;
   ep.obs = obs;
   ep.obs_stride = obs_stride;
