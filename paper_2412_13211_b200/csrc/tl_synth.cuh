@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
       t.seed = seed ^ 0x5EED;
       t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
       p.scripts[e] = t;
+      if (p.ev_off) p.ev_state[e] = 0ull;  // event look-back status of this launch
       if (p.out.rec_start) {  // record layout (tl_fuzz); the env reset has none
         p.out.rec_start[e] = e * p.cap_per_env;
         p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;

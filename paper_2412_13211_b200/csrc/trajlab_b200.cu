@@ -398,8 +398,7 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   if (ev_off) {  // tl_fuzz_ev: fused ordered event lists
     sp.ev_off = ev_off;
     sp.ev_kind = ev_kind;
-    sp.ev_t = ev_t;
-    if (cudaMemsetAsync(sp.ev_state, 0, n * 8, S(stream))) return TL_E_CUDA;
+    sp.ev_t = ev_t;  // ev_state is zeroed by the reset kernel (no memset node)
   }
   return launch_synth(sp, true, stream);
 }
