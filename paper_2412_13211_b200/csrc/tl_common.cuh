@@ -212,6 +212,13 @@ __device__ __forceinline__ double rand53(uint32_t w0, uint32_t w1) {
 }
 
 // Lib/random.py uniform: a + (b - a) * random(), no FMA
+// the same with b - a supplied (constant spans are folded at compile time
+// with the identical IEEE round-to-nearest subtraction CPython performs)
+__device__ __forceinline__ double uniform_span(double a, double span, double r) {
+  return __dadd_rn(a, __dmul_rn(span, r));
+}
+#define TL_UNIFORM(a, b, r) ::tl::uniform_span((a), (double)(b) - (double)(a), (r))
+
 __device__ __forceinline__ double uniform_rn(double a, double b, double r) {
   return __dadd_rn(a, __dmul_rn(__dsub_rn(b, a), r));
 }

@@ -196,7 +196,7 @@ __device__ __forceinline__ void env_emit(const EnvParams& p, EnvSt& s, const RzC
 #pragma unroll
   for (int i = 0; i < DOFMAX; i++) {
     if (i < dof) {
-      const float q = emit ? __double2float_rn(uniform_rn(-0.3, 0.3, env_rand(mt, idx, j0 + 2 * i, so, ss))) : 0.f;
+      const float q = emit ? __double2float_rn(TL_UNIFORM(-0.3, 0.3, env_rand(mt, idx, j0 + 2 * i, so, ss))) : 0.f;
       dst[(int64_t)i * st] = q;
       mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
       if (!c.rest_zero) {
@@ -208,20 +208,20 @@ __device__ __forceinline__ void env_emit(const EnvParams& p, EnvSt& s, const RzC
 #pragma unroll
   for (int i = 0; i < DOFMAX; i++) {
     if (i < dof) {
-      const float qd = emit ? __double2float_rn(uniform_rn(-0.4, 0.4, env_rand(mt, idx, j0 + 2 * (dof + i), so, ss))) : 0.f;
+      const float qd = emit ? __double2float_rn(TL_UNIFORM(-0.4, 0.4, env_rand(mt, idx, j0 + 2 * (dof + i), so, ss))) : 0.f;
       dst[(int64_t)(dof + i) * st] = qd;
       mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
     }
   }
   const int k2 = 2 * dof;
-  auto draw = [&](int k, double a, double b) -> float {
-    return emit ? __double2float_rn(uniform_rn(a, b, env_rand(mt, idx, j0 + 2 * (k2 + k), so, ss))) : 0.f;
+  auto draw = [&](int k, double a, double span) -> float {
+    return emit ? __double2float_rn(uniform_span(a, span, env_rand(mt, idx, j0 + 2 * (k2 + k), so, ss))) : 0.f;
   };
-  v.tor = draw(0, -0.05, 0.05);
-  v.vx = draw(1, -0.2, 0.2);
-  v.vy = draw(2, -0.2, 0.2);
-  v.om = draw(3, -0.3, 0.3);
-  v.der = draw(4, 0.2, 1.0);
+  v.tor = draw(0, -0.05, 0.05 - -0.05);
+  v.vx = draw(1, -0.2, 0.2 - -0.2);
+  v.vy = draw(2, -0.2, 0.2 - -0.2);
+  v.om = draw(3, -0.3, 0.3 - -0.3);
+  v.der = draw(4, 0.2, 1.0 - 0.2);
   const float fnan = __int_as_float(0x7fc00000);
   v.dist = z.has_goal ? __double2float_rn(s.dist) : fnan;
   v.force = z.has_force ? __double2float_rn(s.force) : fnan;
@@ -533,15 +533,15 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
         continue;
       }
       const int kf = d - pre;  // plane
-      double lo, hi;
-      if (kf < dof) { lo = -0.3; hi = 0.3; }
-      else if (kf < 2 * dof) { lo = -0.4; hi = 0.4; }
+      double lo, span;  // rng.uniform bounds of plane kf, b - a folded at compile time
+      if (kf < dof) { lo = -0.3; span = 0.3 - -0.3; }
+      else if (kf < 2 * dof) { lo = -0.4; span = 0.4 - -0.4; }
       else {
         const int j = kf - 2 * dof;
         lo = j == 0 ? -0.05 : j == 3 ? -0.3 : j == 4 ? 0.2 : -0.2;
-        hi = j == 0 ? 0.05 : j == 3 ? 0.3 : j == 4 ? 1.0 : 0.2;
+        span = j == 0 ? 0.05 - -0.05 : j == 3 ? 0.3 - -0.3 : j == 4 ? 1.0 - 0.2 : 0.2 - -0.2;
       }
-      const float v = emit ? __double2float_rn(uniform_rn(lo, hi, r)) : 0.f;
+      const float v = emit ? __double2float_rn(uniform_span(lo, span, r)) : 0.f;
       p.obs[(int64_t)kf * st + col] = v;
       if (kf < dof) {
         mq = fmaxf(mq, fabsf(v));  // generated values are never NaN: max is order-free
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
     if (a == TL_EV_EXCESSIVE_COLLISIONS) s.cum = z.L105;                 // synth.py:210-213
     if (app) {
       const double rd = __shfl_sync(qmask, r_pre, qbase + adv);
-      s.dist = a == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rd) : uniform_rn(0.3, 0.8, rd);
+      s.dist = a == TL_EV_OBJ_AT_GOAL ? TL_UNIFORM(0.02, 0.12, rd) : TL_UNIFORM(0.3, 0.8, rd);
     }
     s.t += 1;
     const float vdist = z.has_goal ? __double2float_rn(s.dist) : fnan;

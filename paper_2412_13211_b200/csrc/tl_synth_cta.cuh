@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         if (emitter) S.radv[et] = valid && adv ? rnd(o) : 0.0;
         if (valid && app) {
           const double rr = rnd(o + 2 * adv);
-          S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? uniform_rn(0.02, 0.12, rr) : uniform_rn(0.3, 0.8, rr);
+          S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? TL_UNIFORM(0.02, 0.12, rr) : TL_UNIFORM(0.3, 0.8, rr);
         }
         if (tid == 0) S.misc[13] = 0x7fffffff;
         __syncthreads();
@@ -456,9 +456,10 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
           const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
           float* __restrict__ dst = P + rr;
           // branch-free: every draw is computed, at-rest records select 0
-          auto draw = [&](uint32_t k, double a, double b) -> float {
+          // rng.uniform(a, b) with b - a folded at compile time (same RN result)
+          auto draw = [&](uint32_t k, double a, double span) -> float {
             const uint2 wv = ring2[((eo + 2u * k) & kMask) >> 1];
-            const float v = __double2float_rn(uniform_rn(a, b, rand53(wv.x, wv.y)));
+            const float v = __double2float_rn(uniform_span(a, span, rand53(wv.x, wv.y)));
             return emit ? v : 0.f;
           };
           RecV<float> v;
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
 #pragma unroll
           for (int i = 0; i < DOFMAX; i++) {
             if (i < dof) {
-              const float q = draw(i, -0.3, 0.3);
+              const float q = draw(i, -0.3, 0.3 - -0.3);
               *dst = q;
               dst += stride;
               mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
@@ -475,18 +476,18 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
 #pragma unroll
           for (int i = 0; i < DOFMAX; i++) {
             if (i < dof) {
-              const float qd = draw(dof + i, -0.4, 0.4);
+              const float qd = draw(dof + i, -0.4, 0.4 - -0.4);
               *dst = qd;
               dst += stride;
               mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
             }
           }
           const uint32_t k2 = 2 * dof;
-          v.tor = draw(k2, -0.05, 0.05);
-          v.vx = draw(k2 + 1, -0.2, 0.2);
-          v.vy = draw(k2 + 2, -0.2, 0.2);
-          v.om = draw(k2 + 3, -0.3, 0.3);
-          v.der = draw(k2 + 4, 0.2, 1.0);
+          v.tor = draw(k2, -0.05, 0.05 - -0.05);
+          v.vx = draw(k2 + 1, -0.2, 0.2 - -0.2);
+          v.vy = draw(k2 + 2, -0.2, 0.2 - -0.2);
+          v.om = draw(k2 + 3, -0.3, 0.3 - -0.3);
+          v.der = draw(k2 + 4, 0.2, 1.0 - 0.2);
           v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
           v.force = stv.force;
           v.cum = 0.f;  // over = false here; cum_patch_bits applies the real value
