@@ -343,3 +343,42 @@ def test_nccl_exchange_entry_points_single_rank():
         assert torch.equal(out, lab) and torch.equal(counts, want)
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+def test_c_abi_rejects_invalid_arguments():
+    """Every entry point validates its arguments and returns TL_E_INVALID
+    (no launch, no crash) for null required pointers / bad sizes."""
+    import ctypes
+    from paper_2412_13211_b200 import _lib as L
+    lib = L.lib()
+    E = L.E_INVALID
+    th = L.Thresholds_c()
+    cfg = L.FuzzCfg_c(8, 4, 5, 0, 1.0, 0.5)
+    bad_cfg = L.FuzzCfg_c(8, 0, 5, 0, 1.0, 0.5)   # max_gap < 1
+    rec = L.Records_c(None, None, None, None, 0, 0, 7)
+    bad_rec = L.Records_c(None, None, None, None, 0, 0, 99)  # dof > 16
+    nul = None
+    assert lib.tl_label_records(None, 1, nul, nul, 1, None, nul, nul, nul, nul) == E
+    assert lib.tl_label_records(ctypes.byref(bad_rec), 1, nul, nul, 1, None, nul, nul, nul, nul) == E
+    assert lib.tl_fuzz(nul, 4, 0, ctypes.byref(bad_cfg), ctypes.byref(th), nul, None,
+                       ctypes.byref(rec), 64, nul, nul, nul, nul, nul, nul, nul) == E
+    assert lib.tl_fuzz(nul, 4, 7, ctypes.byref(cfg), ctypes.byref(th), nul, None,
+                       ctypes.byref(rec), 64, nul, nul, nul, nul, nul, nul, nul) == E
+    assert lib.tl_fuzz_ev(nul, 4, 0, ctypes.byref(cfg), ctypes.byref(th), nul, None,
+                          ctypes.byref(rec), 64, nul, nul, nul, nul, nul, nul, nul, nul, 0,
+                          nul, nul) == E
+    assert lib.tl_realize(nul, nul, nul, 4, ctypes.byref(th), nul, None, ctypes.byref(rec),
+                          nul, nul, nul, nul) == E
+    assert lib.tl_scan_emit_events(nul, nul, nul, nul, 4, nul, nul, nul, nul, nul) == E
+    assert lib.tl_filter_select(nul, 4, 1, 1, nul, nul, 1, nul, nul, nul, nul) == E
+    assert lib.tl_env_reset(nul, 4, 7, nul, ctypes.byref(th), nul, nul, 0, nul, nul, nul) == E
+    assert lib.tl_env_step(nul, 4, 7, nul, 1, nul, 0, nul, nul, nul) == E
+    assert lib.tl_env_labels(nul, 4, None, nul, nul, nul) == E
+    assert lib.tl_env_script_actions(nul, nul, nul, 4, 0, 1, nul, nul) == E
+    assert lib.tl_group_mode_counts(nul, nul, 4, 1, nul, nul) == E
+    assert lib.tl_chain_progress(nul, nul, 4, 99, nul, nul) == E
+    assert lib.tl_filter_buckets(nul, nul, 4, nul, nul, nul, 9, nul, nul) == E
+    assert lib.tl_allgather_labels(nul, nul, 4, nul, nul) == E
+    assert lib.tl_allreduce_counts(nul, nul, 4, nul) == E
+    assert lib.tl_mode_histogram(nul, 4, nul, nul) == E
+    assert lib.tl_status_name(E).decode() != ""
