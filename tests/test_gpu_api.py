@@ -382,3 +382,37 @@ def test_c_abi_rejects_invalid_arguments():
     assert lib.tl_allreduce_counts(nul, nul, 4, nul) == E
     assert lib.tl_mode_histogram(nul, 4, nul, nul) == E
     assert lib.tl_status_name(E).decode() != ""
+
+
+def test_label_batch_and_json_match_reference(tmp_path):
+    """label_batch over TRJL files (GPU labelling) == the reference's
+    BatchResult: canonical LabelRecord JSON, per-file errors, mode counts
+    (tests/golden/labels.json.gz, make_labels_golden.py)."""
+    import io
+    import json
+    import os
+    import paper_2412_13211_b200 as P
+    from golden_data import js
+    g = js("labels")
+    paths = []
+    for name, hx in g["files"].items():
+        pth = tmp_path / name
+        pth.write_bytes(bytes.fromhex(hx))
+        paths.append(str(pth))
+    res = P.label_batch(paths)
+    got = []
+    for r in res.labels:
+        d = r.to_dict()
+        d["source"] = os.path.relpath(d["source"], str(tmp_path))
+        got.append(json.dumps(d, sort_keys=True))
+    assert got == g["labels"]
+    assert [{"source": os.path.relpath(e["source"], str(tmp_path)), "error": e["error"]}
+            for e in res.errors] == g["errors"]
+    assert res.mode_counts == g["mode_counts"]
+    for name, want in g["per_file"].items():
+        data = bytes.fromhex(g["files"][name])
+        try:
+            out = P.label_trajectory(P.read_binary(io.BytesIO(data))).to_json()
+        except Exception as e:  # noqa: BLE001
+            out = f"{type(e).__name__}: {e}"
+        assert out == want, name
