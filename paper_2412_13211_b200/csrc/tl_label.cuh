@@ -500,9 +500,9 @@ __device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, i
     uint32_t ind[4], err[4], m[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      ind[j] = 0;
-      err[j] = 0;
-      if (tb + j < n) {
+      // branch-free: every lane evaluates its 4 slots, invalid ones are masked
+      const bool valid = tb + j < n;
+      {
         RecV<float> v;
         v.der = f4get(der, j);
         v.cum = f4get(cum, j);
@@ -526,7 +526,10 @@ __device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, i
           v.art = f4get(art, j);
         }
         record_bits(c, v, sc_ru, sc_d, ind[j], err[j]);
-        if (step_success) step_success[r + j] = (err[j] & ERR_SUCC) ? 2 : ((ind[j] & IND_SUCCESS) ? 1 : 0);
+        ind[j] = valid ? ind[j] : 0u;
+        err[j] = valid ? err[j] : 0u;
+        if (step_success && valid)
+          step_success[r + j] = (err[j] & ERR_SUCC) ? 2 : ((ind[j] & IND_SUCCESS) ? 1 : 0);
       }
     }
     uint32_t prev = __shfl_up_sync(kFull, ind[3], 1);
@@ -537,8 +540,14 @@ __device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, i
       const bool ok = tb + j < n && tb + j > 0;
       m[j] = ok ? edge_mask(sub, j == 0 ? prev : ind[j - 1], ind[j]) : 0u;
       cnt += __popc(m[j]);
-      eor |= (tb + j < n) ? err[j] : 0u;
-      if (step_mask && tb + j < n) step_mask[r + j] = (uint8_t)m[j];
+      eor |= err[j];
+    }
+    if (step_mask && any) {
+      if (tb + 3 < n) {  // one 4-byte store for the lane's 4 masks
+        *reinterpret_cast<unsigned int*>(step_mask + r) = m[0] | (m[1] << 8) | (m[2] << 16) | (m[3] << 24);
+      } else {
+        for (int j = 0; j < 4 && tb + j < n; j++) step_mask[r + j] = (uint8_t)m[j];
+      }
     }
     const int incl = warp_incl_scan((int)cnt);
     const int excl = incl - (int)cnt;
