@@ -369,6 +369,38 @@ def L_LABEL_DTYPE():
     return _lib.LABEL_DTYPE
 
 
+def label_batch_files_run(n_files=1000):
+    """File-level API (tests/test_acceptance.py C8 shape):
+    label_batch over 1000 TRJL1 files of 200 Pick records each -- host
+    ingestion (one numpy view per file) + one GPU labelling batch + LabelRecords.
+    Wall clock (host work included), best of 3."""
+    import tempfile
+    import paper_2412_13211_b200 as P
+    script = P.EventScript(P.SubtaskKind.Pick, [P.ScriptStep(P.EventKind.Contact, 60),
+                                                P.ScriptStep(P.EventKind.Grasped, 60),
+                                                P.ScriptStep(P.EventKind.Success, 60)], tail=19)
+    trajs = P.realize_many([script] * n_files, list(range(n_files)))
+    with tempfile.TemporaryDirectory() as d:
+        paths = []
+        for i, t in enumerate(trajs):
+            t.header.episode_id = f"ep-{i:06d}"
+            pth = os.path.join(d, f"{i:06d}.trjl")
+            P.write_binary_file(t, pth)
+            paths.append(pth)
+        P.label_batch(paths[:16])
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            res = P.label_batch(paths)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+    assert len(res.labels) == n_files and not res.errors
+    return {"workload": f"label_batch over {n_files} TRJL1 files x 200 records (Pick, C8 shape)",
+            "seconds": best, "files_per_s": n_files / best,
+            "env_steps_per_s": n_files * 200 / best,
+            "reference_note": "the reference takes 0.83 s for this (BASELINE.md C8, 1 worker)"}
+
+
 def c4_run(dev, stream, world, n_chain=4096, reps=3):
     """C4: SetTable chains, 4096 per GPU; chain c runs Open,
     Pick, Place, Close twice with seeds 8c + k (k = 0..7); slot success =
@@ -636,6 +668,7 @@ def main():
         c3 = c3_run(dev, stream, world)
         c5 = c5_run(dev, stream, world)
         c4 = c4_run(dev, stream, world)
+        lbf = label_batch_files_run() if rank == 0 else None
     clk = clocks.summary()
 
     recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
@@ -702,6 +735,7 @@ def main():
         "c3": c3,
         "c5": c5,
         "c4": c4,
+        "label_batch_files": lbf,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
                          "sample": cb_sample, "trajectories_per_sec": cb_eps},
         "clocks": clk,

@@ -172,6 +172,47 @@ def pack_trajectories(trajs, th_base: Optional[Thresholds] = None, force_f64=Fal
     return rb, torch.from_numpy(env_cset).to(dev), table.to_device(dev), len(table)
 
 
+def pack_record_arrays(items, th_base: Optional[Thresholds] = None):
+    """(TrajectoryHeader, TRJL structured record array) pairs -> f32 RecordBatch
+    + csets, with no per-record Python objects: each field is one strided
+    numpy copy into its plane (TRJL1 batched ingestion, io_binary.py:51-104).
+    Episodes start on 4-record boundaries (128-bit label loads)."""
+    torch = _torch()
+    dev = L.device()
+    th_base = th_base or Thresholds()
+    dof = items[0][0].arm_dof if items else 7
+    n_rec = np.array([len(a) for _, a in items], np.int64)
+    n_pad = (n_rec + 3) & ~3
+    rec_start = np.zeros(len(items), np.int64)
+    if len(items) > 1:
+        rec_start[1:] = np.cumsum(n_pad[:-1])
+    R = int(n_pad.sum())
+    F = 2 * dof + 9
+    planes = np.zeros((F, max(R, 4)), np.float32)
+    grasped = np.zeros(max(R, 4), np.uint8)
+    table = CsetTable()
+    env_cset = np.zeros(len(items), np.int32)
+    for i, (h, arr) in enumerate(items):
+        if h.arm_dof != dof:
+            raise ValueError("all trajectories of a batch must share arm_dof")
+        if len(h.rest_arm) != dof:
+            raise ValueError(f"joint vector length mismatch: {dof} vs {len(h.rest_arm)}")
+        r, n = int(rec_start[i]), len(arr)
+        if n:
+            planes[0:dof, r:r + n] = arr["q_arm"].T
+            planes[dof:2 * dof, r:r + n] = arr["qd_arm"].T
+            for j, f in enumerate(SCALAR_FIELDS):
+                planes[2 * dof + j, r:r + n] = arr[f]
+            grasped[r:r + n] = arr["grasped"] != 0
+        env_cset[i] = table.add(SUBTASK_ORDER.index(h.subtask_kind),
+                                ART_ORDER.index(h.articulation_kind), h.art_qmin,
+                                h.art_qmax, dof, h.rest_arm, h.rest_tor, h.thresholds(th_base))
+    rb = RecordBatch(torch.from_numpy(planes).to(dev), torch.from_numpy(grasped).to(dev),
+                     torch.from_numpy(rec_start).to(dev),
+                     torch.from_numpy(n_rec.astype(np.int32)).to(dev), dof)
+    return rb, torch.from_numpy(env_cset).to(dev), table.to_device(dev), len(table)
+
+
 def rules_c(rules_ids) -> Optional[L.Rules_c]:
     """[(subtask, branch, [mode ids])] -> tl_rules (None = reference tables)."""
     if rules_ids is None:

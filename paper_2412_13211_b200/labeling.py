@@ -29,21 +29,35 @@ class Labelled:
 
 
 def label_many(trajs, th: Optional[Thresholds] = None, rules=None, classify=True):
-    from .events import EVENT_KINDS, Event, EventList
-    from .modes import MODE_LIST
     th = th or Thresholds()
     if not trajs:
         return []
     rb, env, cs, n_cs = core.pack_trajectories(trajs, th)
-    res = core.label_records(rb, env, cs, n_cs, rules=rules)
+    return _collect(core.label_records(rb, env, cs, n_cs, rules=rules),
+                    [t.header for t in trajs])
+
+
+def label_arrays(items, th: Optional[Thresholds] = None, rules=None):
+    """label_many for (header, TRJL structured record array) pairs: the file
+    path of label_batch, no per-record Python objects (core.pack_record_arrays)."""
+    th = th or Thresholds()
+    if not items:
+        return []
+    rb, env, cs, n_cs = core.pack_record_arrays(items, th)
+    return _collect(core.label_records(rb, env, cs, n_cs, rules=rules), [h for h, _ in items])
+
+
+def _collect(res, headers):
+    from .events import EVENT_KINDS, Event, EventList
+    from .modes import MODE_LIST
     lab = res.labels_np()
     off = res.ev_off.cpu().numpy()
     kinds = res.ev_kind.cpu().numpy()
     ts = res.ev_t.cpu().numpy()
     out = []
-    for i, traj in enumerate(trajs):
+    for i, hdr in enumerate(headers):
         st = int(lab["status"][i])
-        sub = traj.header.subtask_kind
+        sub = hdr.subtask_kind
         if st != 0 and st != L.ERR_MODE_COVERAGE:
             out.append(Labelled(error=label_error(st, sub.value)))
             continue
