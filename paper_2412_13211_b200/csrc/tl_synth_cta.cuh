@@ -32,7 +32,7 @@ struct CtaCfg {
 
 template <int DOFMAX>
 struct CtaSmem {
-  uint32_t mt[kMtN];
+  uint32_t mt[2][kMtN];  // double-buffered MT state (current block, next block)
   uint32_t wb[CtaCfg<DOFMAX>::kRing];
   int32_t gap[kMaxSteps];
   int32_t tau[kMaxSteps];
@@ -93,6 +93,44 @@ __device__ __forceinline__ void mt_twist_block(uint32_t* mt, uint32_t* ring, uin
   twist_phase4<DOFMAX, 0, 56>(mt, ring, base);
   twist_phase4<DOFMAX, 56, 112>(mt, ring, base);
   twist_phase4<DOFMAX, 112, 156>(mt, ring, base);
+}
+
+// Double-buffered form: the new block is written to `nw` while every old
+// word stays readable in `od`, so a phase needs no barrier between its loads
+// and its stores (no write-after-read hazard): 3 barriers per 624-word block.
+// Word i reads od[i], od[i+1] (nw[0] for i = 623) and od[i+397] (i < 227) or
+// nw[i-227] (i >= 227, written by an earlier phase).
+template <int DOFMAX, int G0, int G1>
+__device__ __forceinline__ void twist_phase_db(const uint32_t* od, uint32_t* nw, uint32_t* ring,
+                                               uint32_t base) {
+  static_assert(G1 - G0 <= kCtaThreads, "one group per thread");
+  const int g = G0 + threadIdx.x;
+  if (g < G1) {
+    const uint4 cur = reinterpret_cast<const uint4*>(od)[g];
+    const int i = 4 * g;
+    const uint32_t nxt = i + 4 == kMtN ? nw[0] : od[i + 4];
+    auto src = [&](int k) {
+      const int ii = i + k;
+      return ii < kMtN - kMtM ? od[ii + kMtM] : nw[ii - (kMtN - kMtM)];
+    };
+    uint4 nv;
+    nv.x = mt_mix(cur.x, cur.y, src(0));
+    nv.y = mt_mix(cur.y, cur.z, src(1));
+    nv.z = mt_mix(cur.z, cur.w, src(2));
+    nv.w = mt_mix(cur.w, nxt, src(3));
+    reinterpret_cast<uint4*>(nw)[g] = nv;
+    const uint4 tv = make_uint4(mt_temper(nv.x), mt_temper(nv.y), mt_temper(nv.z), mt_temper(nv.w));
+    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX>::kMask) >> 2] = tv;
+  }
+  __syncthreads();
+}
+
+template <int DOFMAX>
+__device__ __forceinline__ void mt_twist_block_db(const uint32_t* od, uint32_t* nw, uint32_t* ring,
+                                                  uint32_t base) {
+  twist_phase_db<DOFMAX, 0, 56>(od, nw, ring, base);
+  twist_phase_db<DOFMAX, 56, 112>(od, nw, ring, base);
+  twist_phase_db<DOFMAX, 112, 156>(od, nw, ring, base);
 }
 
 __device__ __forceinline__ int block_max(int v, int32_t* red) {
@@ -205,7 +243,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
       rs = p.out.rec_start[e];
       n_rec = p.out.n_rec[e];
       const uint32_t* src = p.states + (int64_t)e * kMtN;
-      for (int i = tid; i < kMtN; i += kCtaThreads) S.mt[i] = src[i];
+      for (int i = tid; i < kMtN; i += kCtaThreads) S.mt[0][i] = src[i];
     }
     if (FUZZ && sc.n_steps < 0) {
       if (tid == 0) {
@@ -271,6 +309,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
     int32_t w_carry = 2 * z.ne;
     int32_t tau_prev = 0;
     uint32_t produced = 0;
+    int mt_cur = 0;  // which S.mt buffer holds the current block
     int err_code = 0, err_step = -1;
     int s_base = 0;
     const int n_steps = sc.n_steps;
@@ -366,7 +405,8 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         const int wbase = 20 + 8 * min(wave_no, 12);  // profiling build only
         if (tid == 0 && e == 0) TL_STAMP(wbase);
         while ((int)produced < need_max) {
-          mt_twist_block<DOFMAX>(S.mt, S.wb, produced);
+          mt_twist_block_db<DOFMAX>(S.mt[mt_cur], S.mt[mt_cur ^ 1], S.wb, produced);
+          mt_cur ^= 1;
           produced += kMtN;
         }
         if (tid == 0 && e == 0) TL_STAMP(wbase + 1);
