@@ -141,8 +141,7 @@ __device__ __forceinline__ int block_max(int v, int32_t* red) {
   int m = red[0];
 #pragma unroll
   for (int w = 1; w < kCtaThreads / 32; w++) m = max(m, red[w]);
-  __syncthreads();
-  return m;
+  return m;  // red is rewritten only after later barriers of the wave
 }
 
 // ---- fused event lists ---------------------------------------------------------
@@ -440,16 +439,10 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
           }
         }
         if (valid && perr && ev >= 0 && s == pstep && !my_err) my_err = perr;
+        // the wave's InfeasibleScript verdict is read after the next barrier:
+        // an erroneous wave's emission only writes inside the failed episode's
+        // own record slot, and nothing of it is folded
         if (my_err) atomicMin(&S.misc[13], ((s_base + s) << 8) | my_err);
-        __syncthreads();
-        {
-          const int ek = S.misc[13];
-          if (ek != 0x7fffffff) {
-            err_code = ek & 0xff;
-            err_step = ek >> 8;
-            break;
-          }
-        }
         const int cnt = min(kWave, r_end - r0);
         if (!emitter) {
           // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213),
@@ -550,6 +543,14 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
           S.eerr[et] = errb;
         }
         __syncthreads();
+        {
+          const int ek = S.misc[13];
+          if (ek != 0x7fffffff) {
+            err_code = ek & 0xff;
+            err_step = ek >> 8;
+            break;
+          }
+        }
         if (tid == 0 && e == 0) TL_STAMP(wbase + 3);
         if (emitter) {
           uint32_t ind = 0, errb = 0, prev = ind_carry;
@@ -588,7 +589,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
             LS.err_any |= q.err_any;
           }
         }
-        __syncthreads();
+        // no barrier: S.part is rewritten only after the next wave's barriers
         if (tid == 0 && e == 0) TL_STAMP(wbase + 5);
         if (e == 0) wave_no++;
       }
