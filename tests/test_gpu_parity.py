@@ -468,3 +468,45 @@ def test_fused_events_zero_copy_host_outputs(C, TH):
     assert torch.equal(h_off, ref.label_result.ev_off.cpu())
     assert torch.equal(h_k[:tot], ref.label_result.ev_kind[:tot].cpu())
     assert torch.equal(h_t[:tot], ref.label_result.ev_t[:tot].cpu())
+
+
+def test_realize_multi_window_scripts(C, TH):
+    """Scripts longer than one plan window (kMaxSteps = 64 steps) against the
+    oracle: the realize kernel re-plans window by window, carrying the
+    realizer state, word offset and object-distance draws across."""
+    from oracle import oracle as O
+    from golden_data import from_oracle_records
+    rng = np.random.default_rng(99)
+    scripts, seeds = [], []
+    cycles = {0: [0, 1, 2], 1: [3, 6], 2: [8, 7, 9]}  # Pick C,G,D; Place OAG,OLG; Open SO,O,C
+    for i in range(24):
+        kind = i % 3
+        n_steps = int(rng.integers(65, 200))
+        cyc = cycles[kind]
+        kinds = [cyc[j % len(cyc)] for j in range(n_steps)]
+        gaps = list(rng.integers(1, 5, n_steps))
+        d = dict(subtask=kind, kinds=np.asarray(kinds, np.uint8), gaps=np.asarray(gaps, np.int32),
+                 tail=int(rng.integers(1, 6)), initial_grasped=0, initial_contact=0,
+                 initial_dist_obj_goal=0.5 if kind == 1 else 0.5, initial_level=0,
+                 art_kind=1 if kind == 2 else 0, arm_dof=7)
+        scripts.append(d)
+        seeds.append(int(rng.integers(0, 2**31)))
+    arr, k, g = _scripts_np(C, scripts, seeds)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    sb = C.realize_batch(arr, k, g, TH(), cs)
+    lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    planes = sb.records.planes.cpu().numpy()
+    rs = sb.records.rec_start.cpu().numpy()
+    n_ok = 0
+    for i, d in enumerate(scripts):
+        try:
+            recs = O.realize(d, seeds[i])
+        except O.OracleError as e:
+            assert lab["status"][i] == e.code, (i, lab["status"][i], e.code)
+            assert lab["err"][i] == e.step, (i, lab["err"][i], e.step)
+            continue
+        n_ok += 1
+        assert lab["status"][i] == 0, (i, lab["status"][i])
+        p, _ = from_oracle_records(O, recs)
+        assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), i
+    assert n_ok >= 8
