@@ -92,15 +92,15 @@ __device__ int choices_idx(MtLane& R, const double* w, int n) {
   return lo;
 }
 
-// random_script (synth.py:363-507), lane 0.  Returns n_steps or -1 when the
-// script does not fit kMaxSteps.
+// random_script (synth.py:363-507), one thread.  Returns n_steps, or -1
+// when the script does not fit `cap` steps (never for cap = max_events + 4).
 __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
-                             uint8_t* sk, int32_t* sg, tl_script& sc) {
+                             uint8_t* sk, int32_t* sg, tl_script& sc, int cap) {
   int n = 0;
   bool overflow = false;
   auto push = [&](int ev) {
     const int32_t g = R.randint(1, cfg.max_gap);
-    if (n < kMaxSteps) { sk[n] = (uint8_t)ev; sg[n] = g; n++; } else overflow = true;
+    if (n < cap) { sk[n] = (uint8_t)ev; sg[n] = g; n++; } else overflow = true;
   };
   sc.tail = R.randint(1, cfg.max_tail);                                  // :372
   sc.initial_grasped = 0;
@@ -191,7 +191,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
       for (int i = 0; i < 4; i++) g[i] = R.randint(1, cfg.max_gap);
       const int brk = kind == TL_PICK ? TL_EV_DROPPED : kind == TL_PLACE ? TL_EV_OBJ_LEFT_GOAL
                     : kind == TL_OPEN ? TL_EV_CLOSED : TL_EV_OPEN;
-      if (n < kMaxSteps) { sk[n] = (uint8_t)brk; sg[n] = g[kind]; n++; } else overflow = true;
+      if (n < cap) { sk[n] = (uint8_t)brk; sg[n] = g[kind]; n++; } else overflow = true;
     } else if (suffix == 2) {
       push(TL_EV_EXCESSIVE_COLLISIONS);
     } else if (suffix == 3) {
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
       uint8_t* sk = p.step_kind + e * ms;
       int32_t* sg = p.step_gap + e * ms;
       // at most max_events + 4 = ms steps are ever produced (synth.py:463-505)
-      const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t);
+      const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t, ms);
       int64_t nr = 1;
       for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += sg[i];
       const int64_t tmin = ns > 0 ? 0 : 1;

@@ -367,7 +367,7 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   if (!cfg || !th_realize || !label_csets || !out || !labels || !scratch || n_env < 0 ||
       subtask < 0 || subtask > 3 || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
       cfg->max_gap < 1 || cfg->max_tail < 1 || cfg->max_events < 0 ||
-      cfg->max_events + 4 > kMaxSteps || cap_per_env < 2 || (script_kind && !script_gap) ||
+      cap_per_env < 2 || (script_kind && !script_gap) ||
       (!script_kind && script_gap))
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
@@ -523,7 +523,7 @@ int tl_env_reset_fuzz(void* state, const int64_t* seeds, int32_t n_env, int32_t 
                       uint8_t* step_mask, void* stream) {
   if (!state || !seeds || !cfg || !th_realize || !label_csets || !scripts || !script_kind ||
       !script_gap || n_env < 0 || subtask < 0 || subtask > 3 || cfg->max_gap < 1 ||
-      cfg->max_tail < 1 || cfg->max_events < 0 || cfg->max_events + 4 > kMaxSteps ||
+      cfg->max_tail < 1 || cfg->max_events < 0 ||
       (n_env > 0 && !env_obs_ok(obs, obs_stride, n_env)))
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;

@@ -510,3 +510,28 @@ def test_realize_multi_window_scripts(C, TH):
         p, _ = from_oracle_records(O, recs)
         assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), i
     assert n_ok >= 8
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_fuzz_many_events_vs_oracle(C, TH, kind):
+    """FuzzConfig(max_events=150): scripts of up to 154 steps (several plan
+    windows) sampled and realized on the device == the oracle's fuzz."""
+    from oracle import oracle as O
+    from golden_data import from_oracle_records
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_events=150, max_gap=3, max_tail=4)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 300
+    sb = C.fuzz_batch(np.arange(n) + 1000 * kind, kind, cfg, TH(), cs, want_scripts=True)
+    lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    planes = sb.records.planes.cpu().numpy()
+    rs = sb.records.rec_start.cpu().numpy()
+    ocfg = O.fuzz_cfg(max_events=150, max_gap=3, max_tail=4)
+    long_scripts = 0
+    for i in range(n):
+        sc, recs = O.fuzz(1000 * kind + i, kind, ocfg)
+        long_scripts += len(sc["kinds"]) > 64
+        assert lab["status"][i] == 0, (i, lab["status"][i])
+        p, _ = from_oracle_records(O, recs)
+        assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), i
+    assert long_scripts > 10
