@@ -535,3 +535,25 @@ def test_fuzz_many_events_vs_oracle(C, TH, kind):
         p, _ = from_oracle_records(O, recs)
         assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), i
     assert long_scripts > 10
+
+
+def test_fuzz_extreme_seeds_vs_oracle(C, TH):
+    """Negative seeds (random.Random uses abs(seed)), 1- and 2-word keys
+    around 2^32, and the int64 extremes, against the oracle."""
+    from oracle import oracle as O
+    from golden_data import from_oracle_records
+    from paper_2412_13211_b200.synth import FuzzConfig
+    seeds = [0, 1, -1, -7, 2**32 - 1, 2**32, -(2**32), 2**33 + 5, -(2**40) - 3,
+             2**63 - 1, -(2**63), -(2**63) + 1, 123456789012345, -987654321098]
+    cfg = FuzzConfig()
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    for kind in range(4):
+        sb = C.fuzz_batch(torch.tensor(seeds, dtype=torch.int64, device="cuda"), kind, cfg, TH(), cs)
+        planes = sb.records.planes.cpu().numpy()
+        rs = sb.records.rec_start.cpu().numpy()
+        nr = sb.records.n_rec.cpu().numpy()
+        for i, sd in enumerate(seeds):
+            _, recs = O.fuzz(sd, kind)
+            assert nr[i] == len(recs), (kind, sd)
+            p, _ = from_oracle_records(O, recs)
+            assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), (kind, sd)
