@@ -168,36 +168,55 @@ def run_reference(args, rank, world):
     print(json.dumps(out))
 
 
-def label_sizing_run(L, core, lib, dev, stream, flush, n_env=1 << 19, reps=5):
-    """HBM roofline of the labelling kernel: 2^19 Pick episodes x 200 steps
-    (C1/C8 shape, 1.05e8 env steps, 9.8 GB of f32 planes), records resident
-    in HBM (far larger than L2).  One 4096-episode tile is realized on the
-    GPU and replicated; K1 reads only the fields Pick predicates need."""
+LABEL_READ_BYTES = {"pick": 81.0, "place": 85.0, "open": 88.0, "close": 88.0}
+
+
+def label_sizing_run(L, core, lib, dev, stream, flush, n_env=1 << 20, reps=5, subtask="pick"):
+    """HBM roofline of the labelling kernel (SURVEY 8(d) sizing run): 2^20
+    episodes x 200 steps (2.1e8 env steps, 19.3 GB of f32 planes), records
+    resident in HBM (far larger than L2).  One 4096-episode tile of the
+    subtask's success script respaced to 200 records (C1/C3 shapes: Pick /
+    Place 3 events gap 60, Open / Close 4 events gap 45, tail 19; fridge and
+    drawer alternate) is realized on the GPU and replicated; K1 reads only the
+    fields the subtask's predicates need."""
     import ctypes
     import torch
-    from paper_2412_13211_b200.synth import EventScript, ScriptStep
+    from paper_2412_13211_b200 import synth as SY
     from paper_2412_13211_b200.events import EventKind as E
+    from paper_2412_13211_b200.model import ArticulationKind as A, SubtaskKind as SK
     from paper_2412_13211_b200.thresholds import Thresholds
     from paper_2412_13211_b200 import _lib
     tile = 4096
     T = 200
-    arr = np.zeros(tile, _lib.SCRIPT_DTYPE)
-    kinds = np.tile(np.array([0, 1, 12], np.uint8), tile)   # Contact, Grasped, Success
-    gaps = np.full(3 * tile, 60, np.int32)
+    plan = {"pick": (SK.Pick, [E.Contact, E.Grasped, E.Success], 60, {}),
+            "place": (SK.Place, [E.ObjAtGoal, E.ReleasedAtGoal, E.Success], 60,
+                      {"initial_grasped": True}),
+            "open": (SK.Open, [E.Contact, E.SlightlyOpened, E.Opened, E.Success], 45, {}),
+            "close": (SK.Close, [E.Contact, E.SlightlyClosed, E.Closed, E.Success], 45,
+                      {"initial_art_level": "high"})}[subtask]
+    kind, evs, gap, kw = plan
+    scripts = []
     for i in range(tile):
-        arr[i] = (3 * i, i, 3, 19, 0, 0, 0, 0, 0, 7, 0.5)
+        art = A.Fridge if i % 2 == 0 else A.Drawer
+        scripts.append(SY.EventScript(subtask_kind=kind, steps=[SY.ScriptStep(k, gap) for k in evs],
+                                      tail=19, articulation_kind=art, **kw))
+    arr, kinds, gaps = SY._script_array(scripts, np.arange(tile))
     cs12 = core.synth_csets(Thresholds()).to_device(dev)
     sb = core.realize_batch(arr, kinds, gaps, Thresholds(), cs12)
+    assert int(sb.records.n_rec.min()) == T and int(sb.records.n_rec.max()) == T
     R = n_env * T
     planes = torch.empty((23, R), dtype=torch.float32, device=dev)
     grasped = torch.empty(R, dtype=torch.uint8, device=dev)
     reps_n = n_env // tile
     planes.view(23, reps_n, tile * T).copy_(sb.records.planes[:, :tile * T].unsqueeze(1).expand(23, reps_n, tile * T))
     grasped.view(reps_n, tile * T).copy_(sb.records.grasped[:tile * T].unsqueeze(0).expand(reps_n, tile * T))
+    s_idx = int(arr["subtask"][0])
+    art_idx = torch.from_numpy(np.where(np.arange(tile) % 2 == 0, 1, 2).astype(np.int32))
+    env_tile = s_idx * 3 + (art_idx if s_idx >= 2 else torch.zeros(tile, dtype=torch.int32))
     rec_start = torch.arange(n_env, dtype=torch.int64, device=dev) * T
     n_rec = torch.full((n_env,), T, dtype=torch.int32, device=dev)
     rb = core.RecordBatch(planes, grasped, rec_start, n_rec, 7)
-    env = torch.zeros(n_env, dtype=torch.int32, device=dev)     # cset 0 = Pick
+    env = env_tile.to(dev).repeat(reps_n)                        # synth_csets index
     labels = torch.empty((n_env, 24), dtype=torch.uint8, device=dev)
     mask = torch.empty(R, dtype=torch.uint8, device=dev)
     rbc = rb.c()
@@ -214,19 +233,21 @@ def label_sizing_run(L, core, lib, dev, stream, flush, n_env=1 << 19, reps=5):
         if k >= 2:
             ms.append(a.elapsed_time(b))
     lab = labels.cpu().numpy().reshape(-1).view(_lib.LABEL_DTYPE)
-    assert (lab["status"] == 0).all() and (lab["mode"] == 0).all()  # pick.s1 everywhere
+    want = {"pick": 0, "place": 9, "open": 21, "close": 30}[subtask]  # the s1 mode everywhere
+    assert (lab["status"] == 0).all() and (lab["mode"] == want).all(), np.unique(lab["mode"])
     t = sum(ms) / len(ms) / 1e3
-    read_b = 81.0 * R        # Pick: q 28 + qd 28 + v 8 + w 4 + dist_ee_rest 4 + cum 4 + force 4 + grasped 1
+    # Pick: q 28 + qd 28 + v 8 + w 4 + dist_ee_rest 4 + cum 4 + force 4 + grasped 1
+    read_b = LABEL_READ_BYTES[subtask] * R
     write_b = 1.0 * R + 24.0 * n_env
     hbm, _ = peaks()
     del planes, grasped, mask
-    return {"kernel": "k_label<float,7> (tl_label_records)", "episodes": n_env,
+    return {"kernel": "k_label<float,7> (tl_label_records)", "subtask": subtask, "episodes": n_env,
             "env_steps": R, "avg_launch_ms": 1e3 * t,
             "env_steps_per_s": R / t, "trajectories_per_s": n_env / t,
             "algorithmic_bytes_per_launch": read_b + write_b,
             "achieved_GBps": (read_b + write_b) / t / 1e9, "peak_GBps": hbm,
             "frac": (read_b + write_b) / t / 1e9 / hbm,
-            "note": "81 B/env-step read (Pick fields) + 1 B step mask + 24 B/episode label"}
+            "note": f"{LABEL_READ_BYTES[subtask]:.0f} B/env-step read ({subtask} fields) + 1 B step mask + 24 B/episode label"}
 
 
 def env_api_run(dev, stream, n_env=4096, T=200, reps=10):

@@ -572,6 +572,208 @@ __device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, i
   }
 }
 
+// ---- K1 vector path, compile-time arm_dof ---------------------------------------
+// Same contract as label_vec4 for aligned f32 episodes with a zero rest
+// posture; the arm_dof loop is unrolled so every 128-bit load of a chunk is
+// issued before the first use (one HBM latency per chunk instead of one per
+// loop trip), the episode's cuts live in registers (no generic reloads after
+// the step-mask stores), the predicates are evaluated without short-circuit
+// branches (they are pure compares: same values), and the per-kind fold runs
+// only over the kinds that occur in the chunk (events are sparse).
+struct VCuts {
+  float rest, jarm, jtor, sqd, sv, som, lim, contact, goal, a_cut, b_cut;
+  int sub;
+  bool has_art;
+};
+
+__device__ __forceinline__ VCuts vcuts(const tl_cset& c, float sc_ru) {
+  VCuts k;
+  k.rest = c.rd_rest_radius; k.jarm = c.rd_j_arm; k.jtor = c.rd_j_tor;
+  k.sqd = c.rd_static_qd; k.sv = c.rd_static_v; k.som = c.rd_static_om;
+  k.lim = c.rd_limit; k.contact = c.rd_contact; k.goal = c.rd_goal;
+  k.sub = c.subtask;
+  k.has_art = c.art_kind != TL_ART_NONE;
+  // Open: is_open (>= ru) / slightly_opened (>= ru); Close: is_closed (<= rd) / a_q < ru(a_q0 - 0.05 range)
+  k.a_cut = k.sub == TL_OPEN ? c.ru_open : c.rd_closed;
+  k.b_cut = k.sub == TL_OPEN ? c.ru_slight_open : sc_ru;
+  return k;
+}
+
+__device__ __forceinline__ float4 f4abs(float4 v) {
+  return make_float4(fabsf(v.x), fabsf(v.y), fabsf(v.z), fabsf(v.w));
+}
+__device__ __forceinline__ float4 f4pymax(float4 m, float4 v) {
+  return make_float4(pymax_step(m.x, fabsf(v.x)), pymax_step(m.y, fabsf(v.y)),
+                     pymax_step(m.z, fabsf(v.z)), pymax_step(m.w, fabsf(v.w)));
+}
+
+// RPL consecutive f32 records of one plane, one vector load per lane
+template <int RPL> struct VecT;
+template <> struct VecT<4> { typedef float4 T; typedef unsigned int G; };
+template <> struct VecT<2> { typedef float2 T; typedef unsigned short G; };
+
+template <int RPL>
+__device__ __forceinline__ void ldv(const float* p, float (&x)[RPL]) {
+  typedef typename VecT<RPL>::T V;
+  const V v = __ldcs(reinterpret_cast<const V*>(p));  // streamed once: evict-first
+  const float* f = reinterpret_cast<const float*>(&v);
+#pragma unroll
+  for (int j = 0; j < RPL; j++) x[j] = f[j];
+}
+
+// Python max() of |v_i| (pymax_step chain) as a NaN-ignoring fmaxf chain:
+// pymax keeps a leading NaN and never lets a later NaN win, fmaxf drops NaNs,
+// so the two agree except when v_0 is NaN (then the result is NaN).
+template <int DOF, int RPL>
+__device__ __forceinline__ void pymax_all(const float (&v)[DOF][RPL], float (&m)[RPL]) {
+#pragma unroll
+  for (int j = 0; j < RPL; j++) {
+    float x = fabsf(v[0][j]);
+#pragma unroll
+    for (int i = 1; i < DOF; i++) x = fmaxf(x, fabsf(v[i][j]));
+    m[j] = isnan(v[0][j]) ? v[0][j] : x;
+  }
+}
+
+// record_bits (f32 path, zero rest posture), subtask fixed at compile time,
+// no short-circuit branches (the predicates are pure compares: same values)
+template <int SUB>
+__device__ __forceinline__ void record_bits_s(const VCuts& k, float der, float cum, float vx,
+                                              float vy, float om, float qdm, float jm, float xa,
+                                              float xb, float xc, bool g, uint32_t& ind,
+                                              uint32_t& err) {
+  const bool over = cum > k.lim;
+  const bool rest = !(der > k.rest) & !(jm > k.jarm) & (qdm <= k.sqd) & (fabsf(vx) <= k.sv) &
+                    (fabsf(vy) <= k.sv) & (fabsf(om) <= k.som);
+  ind = ((cum <= k.lim) ? IND_CUM_LE : 0u) | (over ? IND_CUM_GT : 0u);
+  bool succ;
+  if (SUB == TL_PICK) {  // xa = force
+    succ = !over & g & rest;
+    ind |= (xa > k.contact ? IND_CONTACT : 0u) | (g ? IND_GRASPED : 0u);
+    err = isnan(xa) ? ERR_FORCE : 0u;
+  } else if (SUB == TL_PLACE) {  // xa = q_tor, xb = dist_obj_goal
+    const bool trs = !(fabsf(xa) > k.jtor);
+    const bool in = xb <= k.goal;
+    const bool dn = isnan(xb);
+    succ = !over & !g & in & rest & trs;
+    ind |= (g ? IND_GRASPED : 0u) | (in ? IND_A : 0u) | (xb > k.goal ? IND_B : 0u);
+    err = (dn ? ERR_DIST : 0u) | ((!over & !g & dn) ? ERR_SUCC : 0u);
+  } else {  // xa = q_tor, xb = art_q, xc = force
+    const bool trs = !(fabsf(xa) > k.jtor);
+    const bool an = isnan(xb);
+    const bool a = SUB == TL_OPEN ? xb >= k.a_cut : xb <= k.a_cut;
+    const bool b = SUB == TL_OPEN ? xb >= k.b_cut : xb < k.b_cut;
+    succ = !over & k.has_art & a & rest & trs;
+    ind |= (xc > k.contact ? IND_CONTACT : 0u) | (a ? IND_A : 0u) | (b ? IND_B : 0u);
+    err = (isnan(xc) ? ERR_FORCE : 0u) | (an ? ERR_ART : 0u) |
+          ((!over & (!k.has_art | an)) ? ERR_SUCC : 0u);
+  }
+  if (succ) ind |= IND_SUCCESS;
+}
+
+// RPL (4 or 2) consecutive records per lane, chunks of 32*RPL records.
+template <int DOF, int SUB, int RPL>
+__device__ __noinline__ void label_vec_d(const tl_records& R, const tl_cset& c, int64_t rs, int n,
+                                         float sc_ru, LState& S, uint8_t* step_mask,
+                                         uint8_t* step_success) {
+  constexpr int CH = 32 * RPL;
+  typedef typename VecT<RPL>::G G;
+  const int lane = lane_id();
+  constexpr int f0 = 2 * DOF;
+  const float* __restrict__ P = reinterpret_cast<const float*>(R.planes) + rs + RPL * lane;
+  const uint8_t* __restrict__ GP = R.grasped + rs + RPL * lane;
+  const int64_t stride = R.plane_stride;
+  const VCuts k = vcuts(c, sc_ru);
+  constexpr int XA = SUB == TL_PICK ? f0 + 6 : f0;       // force | q_tor
+  constexpr int XB = SUB == TL_PLACE ? f0 + 5 : f0 + 8;  // dist_obj_goal | art_q
+  for (int t0 = 0; t0 < n; t0 += CH) {
+    const int tb = t0 + RPL * lane;          // first record of this lane
+    const float* __restrict__ p = P + t0;
+    uint32_t ind[RPL], err[RPL];
+#pragma unroll
+    for (int j = 0; j < RPL; j++) ind[j] = err[j] = 0u;
+    if (tb < n) {
+      // every load of the chunk issued up front
+      float q[DOF][RPL], qd[DOF][RPL];
+#pragma unroll
+      for (int i = 0; i < DOF; i++) {
+        ldv<RPL>(p + i * stride, q[i]);
+        ldv<RPL>(p + (DOF + i) * stride, qd[i]);
+      }
+      float der[RPL], cum[RPL], vx[RPL], vy[RPL], om[RPL], xa[RPL], xb[RPL], xc[RPL];
+      ldv<RPL>(p + (f0 + 4) * stride, der);
+      ldv<RPL>(p + (f0 + 7) * stride, cum);
+      ldv<RPL>(p + (f0 + 1) * stride, vx);
+      ldv<RPL>(p + (f0 + 2) * stride, vy);
+      ldv<RPL>(p + (f0 + 3) * stride, om);
+      ldv<RPL>(p + XA * stride, xa);
+#pragma unroll
+      for (int j = 0; j < RPL; j++) xb[j] = xc[j] = 0.f;
+      uint32_t g4 = 0;
+      if (SUB != TL_PICK) ldv<RPL>(p + XB * stride, xb);
+      if (SUB == TL_OPEN || SUB == TL_CLOSE) ldv<RPL>(p + (f0 + 6) * stride, xc);
+      if (SUB == TL_PICK || SUB == TL_PLACE) g4 = __ldcs(reinterpret_cast<const G*>(GP + t0));
+      // Python max() of |q_i| and |qd_i| per record (predicates.py:20, :24)
+      float mq[RPL], mqd[RPL];
+      pymax_all<DOF, RPL>(q, mq);
+      pymax_all<DOF, RPL>(qd, mqd);
+#pragma unroll
+      for (int j = 0; j < RPL; j++) {
+        record_bits_s<SUB>(k, der[j], cum[j], vx[j], vy[j], om[j], mqd[j], mq[j], xa[j], xb[j],
+                           xc[j], (g4 >> (8 * j)) & 0xffu, ind[j], err[j]);
+        const bool valid = tb + j < n;
+        ind[j] = valid ? ind[j] : 0u;
+        err[j] = valid ? err[j] : 0u;
+        if (step_success && valid)
+          step_success[rs + tb + j] = (err[j] & ERR_SUCC) ? 2 : ((ind[j] & IND_SUCCESS) ? 1 : 0);
+      }
+    }
+    uint32_t prev = __shfl_up_sync(kFull, ind[RPL - 1], 1);
+    if (lane == 0) prev = S.prev_ind;
+    uint32_t m[RPL], orm = 0, eor = 0, packed = 0;
+#pragma unroll
+    for (int j = 0; j < RPL; j++) {
+      const bool ok = tb + j < n && tb + j > 0;
+      m[j] = ok ? edge_mask(SUB, j == 0 ? prev : ind[j - 1], ind[j]) : 0u;
+      orm |= m[j];
+      eor |= err[j];
+      packed |= m[j] << (8 * j);
+    }
+    if (step_mask && tb < n) {
+      if (tb + RPL - 1 < n) {  // one store for the lane's RPL masks
+        *reinterpret_cast<G*>(step_mask + rs + tb) = (G)packed;
+      } else {
+        for (int j = 0; j < RPL && tb + j < n; j++) step_mask[rs + tb + j] = (uint8_t)m[j];
+      }
+    }
+    orm = __reduce_or_sync(kFull, orm);
+    if (orm) {  // warp-uniform: fold only chunks with events, only the kinds present
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < RPL; j++) cnt += __popc(m[j]);
+      const int incl = warp_incl_scan(cnt);
+      const int excl = incl - cnt;
+      while (orm) {
+        const int kk = __ffs(orm) - 1;
+        orm &= orm - 1;
+        // position (within the lane's events) of the lane's last event of kind kk
+        int pos = -1, before = 0;
+#pragma unroll
+        for (int j = 0; j < RPL; j++) {
+          if ((m[j] >> kk) & 1u) pos = before + __popc(m[j] & ((1u << kk) - 1u));
+          before += __popc(m[j]);
+        }
+        const unsigned bal = __ballot_sync(kFull, pos >= 0);
+        const int L = 31 - __clz(bal);
+        S.last[kk] = S.size + __shfl_sync(kFull, excl + pos, L);
+      }
+      S.size += __shfl_sync(kFull, incl, 31);
+    }
+    S.err_any |= __reduce_or_sync(kFull, eor);
+    S.prev_ind = __shfl_sync(kFull, ind[RPL - 1], 31);
+  }
+}
+
 // one record per lane (any layout, f32 or f64 records, any rest posture)
 template <typename T, int DOFMAX>
 __device__ __forceinline__ void label_scalar(const tl_records& R, const tl_cset& c, int64_t rs, int n,
@@ -641,13 +843,20 @@ __device__ __forceinline__ void label_scalar(const tl_records& R, const tl_cset&
 
 // ---- K1: label_records -------------------------------------------------------
 constexpr int kLabelWarps = 8;
+#ifndef TL_LABEL_RPL
+#define TL_LABEL_RPL 4  // records per lane of the compile-time-dof path
+#endif
+#ifndef TL_LABEL_MINB
+#define TL_LABEL_MINB 4  // f32, arm_dof <= 7: 4 x 8 warps per SM at <= 64 registers
+#endif
 
 template <typename T, int DOFMAX>
-__global__ void __launch_bounds__(kLabelWarps * 32)
+__global__ void __launch_bounds__(kLabelWarps * 32,
+                                  (sizeof(T) == 4 && DOFMAX == 7) ? TL_LABEL_MINB : 2)
     k_label(tl_records R, int n_env, const int32_t* __restrict__ env_cset,
             const tl_cset* __restrict__ csets, tl_rules rules,
             uint8_t* __restrict__ step_mask, uint8_t* __restrict__ step_success,
-            tl_label* __restrict__ labels) {
+            tl_label* __restrict__ labels, int vec_generic) {
   __shared__ tl_cset s_cs[kLabelWarps];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const T* __restrict__ P = reinterpret_cast<const T*>(R.planes);
@@ -686,7 +895,15 @@ __global__ void __launch_bounds__(kLabelWarps * 32)
     // 128-bit loads (k_label_vec4); otherwise one record per lane below.
     if (sizeof(T) == 4 && c.rest_zero && (rs & 3) == 0 && vec_ok &&
         rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride) {
-      label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
+      if (dof == 7 && !vec_generic) {
+        switch (c.subtask) {
+          case TL_PICK: label_vec_d<7, TL_PICK, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          case TL_PLACE: label_vec_d<7, TL_PLACE, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          case TL_OPEN: label_vec_d<7, TL_OPEN, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          default: label_vec_d<7, TL_CLOSE, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+        }
+      } else
+        label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
       if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
       continue;
     }

@@ -206,6 +206,7 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
   // it is slower than the register path + L2 bulk prefetch at the occupancy
   // its buffers allow (profiles/r1_ncu_summary.md), kept for A/B runs.
   const bool use_tma = getenv("TL_LABEL_TMA") != nullptr;
+  const int vgen = getenv("TL_LABEL_V4GEN") != nullptr;  // A/B: runtime-dof vec4 body
   if (recs->dtype == 0 && use_tma) {
     if (small) {
       using SM7 = LabelTmaSmem<7>;
@@ -221,11 +222,11 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
                                                    step_success, labels);
     }
   } else if (recs->dtype == 0) {
-    if (small) k_label<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
-    else k_label<float, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
+    if (small) k_label<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    else k_label<float, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
   } else {
-    if (small) k_label<double, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
-    else k_label<double, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels);
+    if (small) k_label<double, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    else k_label<double, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
   }
   return check_launch();
 }
