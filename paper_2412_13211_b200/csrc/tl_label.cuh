@@ -671,9 +671,12 @@ __device__ __forceinline__ void record_bits_s(const VCuts& k, float der, float c
   if (succ) ind |= IND_SUCCESS;
 }
 
+#ifndef TL_VEC_INL
+#define TL_VEC_INL __forceinline__  // inlined: the running state stays in registers
+#endif
 // RPL (4 or 2) consecutive records per lane, chunks of 32*RPL records.
 template <int DOF, int SUB, int RPL>
-__device__ __noinline__ void label_vec_d(const tl_records& R, const tl_cset& c, int64_t rs, int n,
+__device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, int64_t rs, int n,
                                          float sc_ru, LState& S, uint8_t* step_mask,
                                          uint8_t* step_success) {
   constexpr int CH = 32 * RPL;
@@ -686,6 +689,12 @@ __device__ __noinline__ void label_vec_d(const tl_records& R, const tl_cset& c, 
   const VCuts k = vcuts(c, sc_ru);
   constexpr int XA = SUB == TL_PICK ? f0 + 6 : f0;       // force | q_tor
   constexpr int XB = SUB == TL_PLACE ? f0 + 5 : f0 + 8;  // dist_obj_goal | art_q
+  constexpr int NK = SUB == TL_PICK ? 5 : SUB == TL_PLACE ? 7 : 6;  // alphabet size
+  // running state in registers (static indices only), written back at the end
+  int size = S.size, last[NK];
+  uint32_t prev_ind = S.prev_ind, err_any = S.err_any;
+#pragma unroll
+  for (int kk = 0; kk < NK; kk++) last[kk] = S.last[kk];
   for (int t0 = 0; t0 < n; t0 += CH) {
     const int tb = t0 + RPL * lane;          // first record of this lane
     const float* __restrict__ p = P + t0;
@@ -729,7 +738,7 @@ __device__ __noinline__ void label_vec_d(const tl_records& R, const tl_cset& c, 
       }
     }
     uint32_t prev = __shfl_up_sync(kFull, ind[RPL - 1], 1);
-    if (lane == 0) prev = S.prev_ind;
+    if (lane == 0) prev = prev_ind;
     uint32_t m[RPL], orm = 0, eor = 0, packed = 0;
 #pragma unroll
     for (int j = 0; j < RPL; j++) {
@@ -753,9 +762,9 @@ __device__ __noinline__ void label_vec_d(const tl_records& R, const tl_cset& c, 
       for (int j = 0; j < RPL; j++) cnt += __popc(m[j]);
       const int incl = warp_incl_scan(cnt);
       const int excl = incl - cnt;
-      while (orm) {
-        const int kk = __ffs(orm) - 1;
-        orm &= orm - 1;
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        if (!((orm >> kk) & 1u)) continue;  // warp-uniform
         // position (within the lane's events) of the lane's last event of kind kk
         int pos = -1, before = 0;
 #pragma unroll
@@ -765,13 +774,18 @@ __device__ __noinline__ void label_vec_d(const tl_records& R, const tl_cset& c, 
         }
         const unsigned bal = __ballot_sync(kFull, pos >= 0);
         const int L = 31 - __clz(bal);
-        S.last[kk] = S.size + __shfl_sync(kFull, excl + pos, L);
+        last[kk] = size + __shfl_sync(kFull, excl + pos, L);
       }
-      S.size += __shfl_sync(kFull, incl, 31);
+      size += __shfl_sync(kFull, incl, 31);
     }
-    S.err_any |= __reduce_or_sync(kFull, eor);
-    S.prev_ind = __shfl_sync(kFull, ind[RPL - 1], 31);
+    err_any |= __reduce_or_sync(kFull, eor);
+    prev_ind = __shfl_sync(kFull, ind[RPL - 1], 31);
   }
+  S.size = size;
+  S.prev_ind = prev_ind;
+  S.err_any = err_any;
+#pragma unroll
+  for (int kk = 0; kk < NK; kk++) S.last[kk] = last[kk];
 }
 
 // one record per lane (any layout, f32 or f64 records, any rest posture)
