@@ -581,21 +581,33 @@ __device__ __noinline__ void label_vec4(const tl_records& R, const tl_cset& c, i
 // branches (they are pure compares: same values), and the per-kind fold runs
 // only over the kinds that occur in the chunk (events are sparse).
 struct VCuts {
-  float rest, jarm, jtor, sqd, sv, som, lim, contact, goal, a_cut, b_cut;
+  float rest_, jarm_, jtor_, sqd_, sv_, som_, lim_, contact_, goal_, a_cut_, b_cut_;
   int sub;
-  bool has_art;
+  bool has_art_;
+  __device__ float rest() const { return rest_; }
+  __device__ float jarm() const { return jarm_; }
+  __device__ float jtor() const { return jtor_; }
+  __device__ float sqd() const { return sqd_; }
+  __device__ float sv() const { return sv_; }
+  __device__ float som() const { return som_; }
+  __device__ float lim() const { return lim_; }
+  __device__ float contact() const { return contact_; }
+  __device__ float goal() const { return goal_; }
+  __device__ float a_cut() const { return a_cut_; }
+  __device__ float b_cut() const { return b_cut_; }
+  __device__ bool has_art() const { return has_art_; }
 };
 
 __device__ __forceinline__ VCuts vcuts(const tl_cset& c, float sc_ru) {
   VCuts k;
-  k.rest = c.rd_rest_radius; k.jarm = c.rd_j_arm; k.jtor = c.rd_j_tor;
-  k.sqd = c.rd_static_qd; k.sv = c.rd_static_v; k.som = c.rd_static_om;
-  k.lim = c.rd_limit; k.contact = c.rd_contact; k.goal = c.rd_goal;
+  k.rest_ = c.rd_rest_radius; k.jarm_ = c.rd_j_arm; k.jtor_ = c.rd_j_tor;
+  k.sqd_ = c.rd_static_qd; k.sv_ = c.rd_static_v; k.som_ = c.rd_static_om;
+  k.lim_ = c.rd_limit; k.contact_ = c.rd_contact; k.goal_ = c.rd_goal;
   k.sub = c.subtask;
-  k.has_art = c.art_kind != TL_ART_NONE;
+  k.has_art_ = c.art_kind != TL_ART_NONE;
   // Open: is_open (>= ru) / slightly_opened (>= ru); Close: is_closed (<= rd) / a_q < ru(a_q0 - 0.05 range)
-  k.a_cut = k.sub == TL_OPEN ? c.ru_open : c.rd_closed;
-  k.b_cut = k.sub == TL_OPEN ? c.ru_slight_open : sc_ru;
+  k.a_cut_ = k.sub == TL_OPEN ? c.ru_open : c.rd_closed;
+  k.b_cut_ = k.sub == TL_OPEN ? c.ru_slight_open : sc_ru;
   return k;
 }
 
@@ -637,40 +649,41 @@ __device__ __forceinline__ void pymax_all(const float (&v)[DOF][RPL], float (&m)
 
 // record_bits (f32 path, zero rest posture), subtask fixed at compile time,
 // no short-circuit branches (the predicates are pure compares: same values)
-template <int SUB>
-__device__ __forceinline__ void record_bits_s(const VCuts& k, float der, float cum, float vx,
+template <int SUB, class K>
+__device__ __forceinline__ void record_bits_s(const K& k, float der, float cum, float vx,
                                               float vy, float om, float qdm, float jm, float xa,
                                               float xb, float xc, bool g, uint32_t& ind,
                                               uint32_t& err) {
-  const bool over = cum > k.lim;
-  const bool rest = !(der > k.rest) & !(jm > k.jarm) & (qdm <= k.sqd) & (fabsf(vx) <= k.sv) &
-                    (fabsf(vy) <= k.sv) & (fabsf(om) <= k.som);
-  ind = ((cum <= k.lim) ? IND_CUM_LE : 0u) | (over ? IND_CUM_GT : 0u);
+  const bool over = cum > k.lim();
+  const bool rest = !(der > k.rest()) & !(jm > k.jarm()) & (qdm <= k.sqd()) & (fabsf(vx) <= k.sv()) &
+                    (fabsf(vy) <= k.sv()) & (fabsf(om) <= k.som());
+  ind = ((cum <= k.lim()) ? IND_CUM_LE : 0u) | (over ? IND_CUM_GT : 0u);
   bool succ;
   if (SUB == TL_PICK) {  // xa = force
     succ = !over & g & rest;
-    ind |= (xa > k.contact ? IND_CONTACT : 0u) | (g ? IND_GRASPED : 0u);
+    ind |= (xa > k.contact() ? IND_CONTACT : 0u) | (g ? IND_GRASPED : 0u);
     err = isnan(xa) ? ERR_FORCE : 0u;
   } else if (SUB == TL_PLACE) {  // xa = q_tor, xb = dist_obj_goal
-    const bool trs = !(fabsf(xa) > k.jtor);
-    const bool in = xb <= k.goal;
+    const bool trs = !(fabsf(xa) > k.jtor());
+    const bool in = xb <= k.goal();
     const bool dn = isnan(xb);
     succ = !over & !g & in & rest & trs;
-    ind |= (g ? IND_GRASPED : 0u) | (in ? IND_A : 0u) | (xb > k.goal ? IND_B : 0u);
+    ind |= (g ? IND_GRASPED : 0u) | (in ? IND_A : 0u) | (xb > k.goal() ? IND_B : 0u);
     err = (dn ? ERR_DIST : 0u) | ((!over & !g & dn) ? ERR_SUCC : 0u);
   } else {  // xa = q_tor, xb = art_q, xc = force
-    const bool trs = !(fabsf(xa) > k.jtor);
+    const bool trs = !(fabsf(xa) > k.jtor());
     const bool an = isnan(xb);
-    const bool a = SUB == TL_OPEN ? xb >= k.a_cut : xb <= k.a_cut;
-    const bool b = SUB == TL_OPEN ? xb >= k.b_cut : xb < k.b_cut;
-    succ = !over & k.has_art & a & rest & trs;
-    ind |= (xc > k.contact ? IND_CONTACT : 0u) | (a ? IND_A : 0u) | (b ? IND_B : 0u);
+    const bool a = SUB == TL_OPEN ? xb >= k.a_cut() : xb <= k.a_cut();
+    const bool b = SUB == TL_OPEN ? xb >= k.b_cut() : xb < k.b_cut();
+    succ = !over & k.has_art() & a & rest & trs;
+    ind |= (xc > k.contact() ? IND_CONTACT : 0u) | (a ? IND_A : 0u) | (b ? IND_B : 0u);
     err = (isnan(xc) ? ERR_FORCE : 0u) | (an ? ERR_ART : 0u) |
-          ((!over & (!k.has_art | an)) ? ERR_SUCC : 0u);
+          ((!over & (!k.has_art() | an)) ? ERR_SUCC : 0u);
   }
   if (succ) ind |= IND_SUCCESS;
 }
 
+constexpr int kLabelWarpsMax = 8;
 #ifndef TL_VEC_INL
 #define TL_VEC_INL __forceinline__  // inlined: the running state stays in registers
 #endif
@@ -690,9 +703,13 @@ __device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, in
   constexpr int XA = SUB == TL_PICK ? f0 + 6 : f0;       // force | q_tor
   constexpr int XB = SUB == TL_PLACE ? f0 + 5 : f0 + 8;  // dist_obj_goal | art_q
   constexpr int NK = SUB == TL_PICK ? 5 : SUB == TL_PLACE ? 7 : 6;  // alphabet size
-  // running state in registers (static indices only), written back at the end
-  int size = S.size, last[NK];
+  // running state in registers, written back at the end
+  int size = S.size;
   uint32_t prev_ind = S.prev_ind, err_any = S.err_any;
+  // last-index state in shared memory (touched only by chunks with events):
+  // keeps registers for the chunk's loads
+  __shared__ int s_last[kLabelWarpsMax][8];
+  int* last = s_last[threadIdx.x >> 5];
 #pragma unroll
   for (int kk = 0; kk < NK; kk++) last[kk] = S.last[kk];
   for (int t0 = 0; t0 < n; t0 += CH) {
@@ -857,6 +874,7 @@ __device__ __forceinline__ void label_scalar(const tl_records& R, const tl_cset&
 
 // ---- K1: label_records -------------------------------------------------------
 constexpr int kLabelWarps = 8;
+static_assert(kLabelWarps <= kLabelWarpsMax, "label_vec_d's per-warp state");
 #ifndef TL_LABEL_RPL
 #define TL_LABEL_RPL 4  // records per lane of the compile-time-dof path
 #endif
