@@ -619,31 +619,14 @@ __device__ __forceinline__ float4 f4pymax(float4 m, float4 v) {
                      pymax_step(m.z, fabsf(v.z)), pymax_step(m.w, fabsf(v.w)));
 }
 
-// RPL consecutive f32 records of one plane, one vector load per lane
-template <int RPL> struct VecT;
-template <> struct VecT<4> { typedef float4 T; typedef unsigned int G; };
-template <> struct VecT<2> { typedef float2 T; typedef unsigned short G; };
-
-template <int RPL>
-__device__ __forceinline__ void ldv(const float* p, float (&x)[RPL]) {
-  typedef typename VecT<RPL>::T V;
-  const V v = __ldcs(reinterpret_cast<const V*>(p));  // streamed once: evict-first
-  const float* f = reinterpret_cast<const float*>(&v);
+template <int DOF>
+__device__ __forceinline__ void pymax4(const float4 (&v)[DOF], float (&m)[4]) {
 #pragma unroll
-  for (int j = 0; j < RPL; j++) x[j] = f[j];
-}
-
-// Python max() of |v_i| (pymax_step chain) as a NaN-ignoring fmaxf chain:
-// pymax keeps a leading NaN and never lets a later NaN win, fmaxf drops NaNs,
-// so the two agree except when v_0 is NaN (then the result is NaN).
-template <int DOF, int RPL>
-__device__ __forceinline__ void pymax_all(const float (&v)[DOF][RPL], float (&m)[RPL]) {
+  for (int j = 0; j < 4; j++) {
+    float x = fabsf(f4get(v[0], j));
 #pragma unroll
-  for (int j = 0; j < RPL; j++) {
-    float x = fabsf(v[0][j]);
-#pragma unroll
-    for (int i = 1; i < DOF; i++) x = fmaxf(x, fabsf(v[i][j]));
-    m[j] = isnan(v[0][j]) ? v[0][j] : x;
+    for (int i = 1; i < DOF; i++) x = fmaxf(x, fabsf(f4get(v[i], j)));
+    m[j] = isnan(f4get(v[0], j)) ? f4get(v[0], j) : x;
   }
 }
 
@@ -687,13 +670,13 @@ constexpr int kLabelWarpsMax = 8;
 #ifndef TL_VEC_INL
 #define TL_VEC_INL __forceinline__  // inlined: the running state stays in registers
 #endif
-// RPL (4 or 2) consecutive records per lane, chunks of 32*RPL records.
-template <int DOF, int SUB, int RPL>
+// 4 consecutive records per lane, chunks of 128 records.
+template <int DOF, int SUB>
 __device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, int64_t rs, int n,
                                          float sc_ru, LState& S, uint8_t* step_mask,
                                          uint8_t* step_success) {
-  constexpr int CH = 32 * RPL;
-  typedef typename VecT<RPL>::G G;
+  constexpr int RPL = 4, CH = 32 * RPL;  // 4 consecutive records per lane
+  typedef unsigned int G;                 // the lane's 4 grasped bytes / step masks
   const int lane = lane_id();
   constexpr int f0 = 2 * DOF;
   const float* __restrict__ P = reinterpret_cast<const float*>(R.planes) + rs + RPL * lane;
@@ -720,29 +703,31 @@ __device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, in
     for (int j = 0; j < RPL; j++) ind[j] = err[j] = 0u;
     if (tb < n) {
       // every load of the chunk issued up front
-      float q[DOF][RPL], qd[DOF][RPL];
+      float4 q[DOF], qd[DOF];
 #pragma unroll
       for (int i = 0; i < DOF; i++) {
-        ldv<RPL>(p + i * stride, q[i]);
-        ldv<RPL>(p + (DOF + i) * stride, qd[i]);
+        q[i] = ldf4(p + i * stride);
+        qd[i] = ldf4(p + (DOF + i) * stride);
       }
-      float der[RPL], cum[RPL], vx[RPL], vy[RPL], om[RPL], xa[RPL], xb[RPL], xc[RPL];
-      ldv<RPL>(p + (f0 + 4) * stride, der);
-      ldv<RPL>(p + (f0 + 7) * stride, cum);
-      ldv<RPL>(p + (f0 + 1) * stride, vx);
-      ldv<RPL>(p + (f0 + 2) * stride, vy);
-      ldv<RPL>(p + (f0 + 3) * stride, om);
-      ldv<RPL>(p + XA * stride, xa);
-#pragma unroll
-      for (int j = 0; j < RPL; j++) xb[j] = xc[j] = 0.f;
+      const float4 der4 = ldf4(p + (f0 + 4) * stride), cum4 = ldf4(p + (f0 + 7) * stride);
+      const float4 vx4 = ldf4(p + (f0 + 1) * stride), vy4 = ldf4(p + (f0 + 2) * stride);
+      const float4 om4 = ldf4(p + (f0 + 3) * stride), xa4 = ldf4(p + XA * stride);
+      float4 xb4 = make_float4(0.f, 0.f, 0.f, 0.f), xc4 = xb4;
       uint32_t g4 = 0;
-      if (SUB != TL_PICK) ldv<RPL>(p + XB * stride, xb);
-      if (SUB == TL_OPEN || SUB == TL_CLOSE) ldv<RPL>(p + (f0 + 6) * stride, xc);
+      if (SUB != TL_PICK) xb4 = ldf4(p + XB * stride);
+      if (SUB == TL_OPEN || SUB == TL_CLOSE) xc4 = ldf4(p + (f0 + 6) * stride);
       if (SUB == TL_PICK || SUB == TL_PLACE) g4 = __ldcs(reinterpret_cast<const G*>(GP + t0));
+      float der[RPL], cum[RPL], vx[RPL], vy[RPL], om[RPL], xa[RPL], xb[RPL], xc[RPL];
+#pragma unroll
+      for (int j = 0; j < RPL; j++) {
+        der[j] = f4get(der4, j); cum[j] = f4get(cum4, j); vx[j] = f4get(vx4, j);
+        vy[j] = f4get(vy4, j); om[j] = f4get(om4, j); xa[j] = f4get(xa4, j);
+        xb[j] = f4get(xb4, j); xc[j] = f4get(xc4, j);
+      }
       // Python max() of |q_i| and |qd_i| per record (predicates.py:20, :24)
       float mq[RPL], mqd[RPL];
-      pymax_all<DOF, RPL>(q, mq);
-      pymax_all<DOF, RPL>(qd, mqd);
+      pymax4<DOF>(q, mq);
+      pymax4<DOF>(qd, mqd);
 #pragma unroll
       for (int j = 0; j < RPL; j++) {
         record_bits_s<SUB>(k, der[j], cum[j], vx[j], vy[j], om[j], mqd[j], mq[j], xa[j], xb[j],
@@ -875,9 +860,6 @@ __device__ __forceinline__ void label_scalar(const tl_records& R, const tl_cset&
 // ---- K1: label_records -------------------------------------------------------
 constexpr int kLabelWarps = 8;
 static_assert(kLabelWarps <= kLabelWarpsMax, "label_vec_d's per-warp state");
-#ifndef TL_LABEL_RPL
-#define TL_LABEL_RPL 4  // records per lane of the compile-time-dof path
-#endif
 #ifndef TL_LABEL_MINB
 #define TL_LABEL_MINB 4  // f32, arm_dof <= 7: 4 x 8 warps per SM at <= 64 registers
 #endif
@@ -929,10 +911,10 @@ __global__ void __launch_bounds__(kLabelWarps * 32,
         rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride) {
       if (dof == 7 && !vec_generic) {
         switch (c.subtask) {
-          case TL_PICK: label_vec_d<7, TL_PICK, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-          case TL_PLACE: label_vec_d<7, TL_PLACE, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-          case TL_OPEN: label_vec_d<7, TL_OPEN, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-          default: label_vec_d<7, TL_CLOSE, TL_LABEL_RPL>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          case TL_PICK: label_vec_d<7, TL_PICK>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          case TL_PLACE: label_vec_d<7, TL_PLACE>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          case TL_OPEN: label_vec_d<7, TL_OPEN>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+          default: label_vec_d<7, TL_CLOSE>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
         }
       } else
         label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
