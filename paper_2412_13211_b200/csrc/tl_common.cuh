@@ -142,6 +142,88 @@ __device__ __forceinline__ void mt_seed_impl(uint32_t* mt, uint32_t k0, uint32_t
   out[0] = 0x80000000u;
 }
 
+// init_by_array without per-thread storage of the first loop's output: the
+// second loop reads first-loop word i exactly once, at position i, in
+// order -- except word 1, which the first loop's 624th iteration rewrites
+// and the second loop reads first.  So pass 1 runs the first loop for its
+// last word and the final word 1 only; pass 2 regenerates the first loop
+// (chain a, the same table reads) in lockstep with the second loop
+// (chain b), two independent dependency chains, and streams the final
+// state to `out` (shared or global).  Same latency as mt_seed_impl, no
+// 2.5 KB working row.
+template <int KLEN>
+__device__ __forceinline__ void mt_seed_stream_impl(uint32_t k0, uint32_t k1, uint32_t* out) {
+  const uint32_t* T = kTlInitGenrand;
+  const uint32_t v1 = seed_step1<KLEN>(T[0], T[1], 1, k0, k1);
+  uint32_t prev = v1;
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) a[k] = T[2 + k];
+  for (int g = 0; g < 76; g += 2) {  // i = 2..609
+    const int i0 = 2 + 8 * g;
+#pragma unroll
+    for (int k = 0; k < 8; k++) b[k] = T[i0 + 8 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) prev = seed_step1<KLEN>(prev, a[k], i0 + k, k0, k1);
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = T[i0 + 16 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) prev = seed_step1<KLEN>(prev, b[k], i0 + 8 + k, k0, k1);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) prev = seed_step1<KLEN>(prev, a[k], 610 + k, k0, k1);
+#pragma unroll
+  for (int k = 0; k < 6; k++) prev = seed_step1<KLEN>(prev, T[618 + k], 618 + k, k0, k1);
+  // mt[0] = mt[623]; 624th iteration: i = 1 (old word = v1), j = 623 % klen
+  const uint32_t m1 = seed_step1<KLEN>(prev, v1, kMtN, k0, k1);
+  auto step2 = [](uint32_t pv, uint32_t old, int i) {
+    return (old ^ ((pv ^ (pv >> 30)) * 1566083941u)) - (uint32_t)i;
+  };
+  uint32_t pa = v1, pb = m1;
+#pragma unroll
+  for (int k = 0; k < 8; k++) a[k] = T[2 + k];
+  for (int g = 0; g < 76; g += 2) {
+    const int i0 = 2 + 8 * g;
+#pragma unroll
+    for (int k = 0; k < 8; k++) b[k] = T[i0 + 8 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      pa = seed_step1<KLEN>(pa, a[k], i0 + k, k0, k1);
+      pb = step2(pb, pa, i0 + k);
+      out[i0 + k] = pb;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = T[i0 + 16 + k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      pa = seed_step1<KLEN>(pa, b[k], i0 + 8 + k, k0, k1);
+      pb = step2(pb, pa, i0 + 8 + k);
+      out[i0 + 8 + k] = pb;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    pa = seed_step1<KLEN>(pa, a[k], 610 + k, k0, k1);
+    pb = step2(pb, pa, 610 + k);
+    out[610 + k] = pb;
+  }
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    pa = seed_step1<KLEN>(pa, T[618 + k], 618 + k, k0, k1);
+    pb = step2(pb, pa, 618 + k);
+    out[618 + k] = pb;
+  }
+  out[1] = step2(pb, m1, 1);  // wrap: mt[0] = mt[623], i = 1 reads the final word 1
+  out[0] = 0x80000000u;
+}
+
+__device__ __noinline__ void mt_seed_lane_stream(int64_t seed, uint32_t* out) {
+  const uint64_t n = seed < 0 ? (uint64_t)0 - (uint64_t)seed : (uint64_t)seed;
+  const uint32_t k0 = (uint32_t)n, k1 = (uint32_t)(n >> 32);
+  if (k1) mt_seed_stream_impl<2>(k0, k1, out);
+  else mt_seed_stream_impl<1>(k0, 0u, out);
+}
+
 // seed one state; the result lands in `out` (== mt for an in-place seed)
 __device__ __noinline__ void mt_seed_lane(uint32_t* mt, int64_t seed, uint32_t* out = nullptr) {
   const uint64_t n = seed < 0 ? (uint64_t)0 - (uint64_t)seed : (uint64_t)seed;
@@ -210,6 +292,19 @@ __device__ __forceinline__ double rand53(uint32_t w0, uint32_t w1) {
   const double r = __longlong_as_double(__double_as_longlong(d) - (53ll << 52));
   return k ? r : 0.0;
 }
+
+// cp.async (global -> shared, no registers in flight)
+__device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Lib/random.py uniform: a + (b - a) * random(), no FMA
 // the same with b - a supplied (constant spans are folded at compile time

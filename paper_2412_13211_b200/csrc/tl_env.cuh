@@ -136,13 +136,7 @@ __device__ __forceinline__ void env_stage(const uint32_t* __restrict__ mt, int i
 // idx' = idx + nw: the window never overlaps the words step k regenerates
 // (they precede idx'; their sources lie >= 227 words behind), so the
 // copies overlap step k's arithmetic.
-__device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// (cp_async4 / cp_async_commit / cp_async_wait: tl_common.cuh)
 
 template <int MAXW>
 __device__ __forceinline__ void env_stage_async(const uint32_t* __restrict__ mt, int idx,

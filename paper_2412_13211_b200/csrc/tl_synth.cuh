@@ -369,21 +369,29 @@ constexpr int kRowWords = kMtN + 1;
 // EPW episodes per warp: lanes 2j / 2j+1 own episode j (script RNG +
 // random_script / realize RNG).  EPW = 1 for small (latency-bound) batches:
 // sampling is serial branchy code, and 16 samplers in one warp diverge.
-template <int EPW>
+// STREAM: both lanes seed with mt_seed_lane_stream (no working row), so only
+// the script lane's final state needs shared memory: EPW rows instead of
+// 2*EPW, twice the warps per SM where shared memory sets the occupancy.
+template <int EPW, bool STREAM>
 __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
-  extern __shared__ uint32_t rows[];  // [2*EPW][kRowWords]
+  extern __shared__ uint32_t rows[];  // [2*EPW or EPW (STREAM)][kRowWords]
   const int lane = lane_id();
   const int64_t e0 = (int64_t)blockIdx.x * EPW;
   const int64_t e = e0 + (lane >> 1);
   const bool valid = (lane >> 1) < EPW && e < p.n_env;
-  uint32_t* row = rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
+  uint32_t* row = STREAM ? rows + (lane < 2 * EPW ? lane >> 1 : 0) * kRowWords
+                         : rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
   const int ms = p.cfg.max_events + 4;
   if (lane == 0) TL_STAMP(0);
   if (valid) {
     const int64_t seed = p.seeds[e];
     // odd lanes: realize RNG, final state written straight to global memory
-    mt_seed_lane(row, (lane & 1) ? (seed ^ 0x5EED) : seed,
-                 (lane & 1) ? p.states + e * kMtN : nullptr);
+    if (STREAM)
+      mt_seed_lane_stream((lane & 1) ? (seed ^ 0x5EED) : seed,
+                          (lane & 1) ? p.states + e * kMtN : row);
+    else
+      mt_seed_lane(row, (lane & 1) ? (seed ^ 0x5EED) : seed,
+                   (lane & 1) ? p.states + e * kMtN : nullptr);
     if (lane == 0) TL_STAMP(1);
     if (!(lane & 1)) {
       MtLane R{row, 0, 0};
@@ -412,13 +420,11 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
   if (lane == 0) TL_STAMP(2);
 }
 
-// realize path: seed the realize RNG of given scripts (one thread per state)
-__global__ void __launch_bounds__(32) k_seed_states(SynthParams p) {
-  extern __shared__ uint32_t rows[];
-  const int lane = lane_id();
-  const int64_t e0 = (int64_t)blockIdx.x * 32;
-  const int64_t e = e0 + lane;
-  if (e < p.n_env) mt_seed_lane(rows + lane * kRowWords, p.scripts[e].seed, p.states + e * kMtN);
+// realize path: seed the realize RNG of given scripts (one thread per state,
+// streamed straight to global memory: no shared memory)
+__global__ void __launch_bounds__(128) k_seed_states(SynthParams p) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < p.n_env) mt_seed_lane_stream(p.scripts[e].seed, p.states + e * kMtN);
 }
 
 }  // namespace tl

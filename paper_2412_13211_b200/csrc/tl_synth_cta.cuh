@@ -50,6 +50,11 @@ struct CtaSmem {
   int32_t misc[16];
   int32_t red[8];
   tl_cset cs;
+  // the CTA's next episode, copied in by cp.async while this one runs
+  alignas(16) uint32_t mt_pf[kMtN];
+  tl_script sc_pf;
+  int64_t rs_pf;
+  int32_t nrec_pf;
 };
 
 // CPython's block regeneration in 4-word groups (group g = words 4g..4g+3).
@@ -231,19 +236,29 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
   const uint2* ring2 = reinterpret_cast<const uint2*>(S.wb);
 
   int wave_no = 0;
+  bool pf = false;  // the next episode's inputs are in flight to S.*_pf
   for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
     if (tid == 0 && e == 0) TL_STAMP(10);
     // ---------------- script + seeded RNG state -------------------------------
     tl_script sc;
     int64_t rs;
     int n_rec;
-    {
+    if (pf) {
+      cp_async_wait<0>();
+      __syncthreads();
+      sc = S.sc_pf;
+      rs = S.rs_pf;
+      n_rec = S.nrec_pf;
+      for (int i = tid; i < kMtN / 4; i += kCtaThreads)
+        reinterpret_cast<uint4*>(S.mt[0])[i] = reinterpret_cast<const uint4*>(S.mt_pf)[i];
+    } else {
       sc = p.scripts[e];
       rs = p.out.rec_start[e];
       n_rec = p.out.n_rec[e];
       const uint32_t* src = p.states + (int64_t)e * kMtN;
       for (int i = tid; i < kMtN; i += kCtaThreads) S.mt[0][i] = src[i];
     }
+    pf = false;
     if (FUZZ && sc.n_steps < 0) {
       if (tid == 0) {
         tl_label L;
@@ -261,6 +276,24 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
     RzConst z;
     const int st0 = realizer_init(z, sc, p.th, dof);
     __syncthreads();
+    {  // S.*_pf are free again (copied out above): fetch the next episode's inputs
+      const int en = e + gridDim.x;
+      if (en < p.n_env) {
+        const uint32_t* src = p.states + (int64_t)en * kMtN;
+        for (int i = tid; i < kMtN / 4; i += kCtaThreads) cp_async16(S.mt_pf + 4 * i, src + 4 * i);
+        if (tid < (int)(sizeof(tl_script) / 4))
+          cp_async4(reinterpret_cast<uint32_t*>(&S.sc_pf) + tid,
+                    reinterpret_cast<const uint32_t*>(&p.scripts[en]) + tid);
+        else if (tid < (int)(sizeof(tl_script) / 4) + 2)
+          cp_async4(reinterpret_cast<uint32_t*>(&S.rs_pf) + (tid - sizeof(tl_script) / 4),
+                    reinterpret_cast<const uint32_t*>(&p.out.rec_start[en]) + (tid - sizeof(tl_script) / 4));
+        else if (tid == (int)(sizeof(tl_script) / 4) + 2)
+          cp_async4(reinterpret_cast<uint32_t*>(&S.nrec_pf),
+                    reinterpret_cast<const uint32_t*>(&p.out.n_rec[en]));
+        cp_async_commit();
+        pf = true;
+      }
+    }
     auto fail = [&](int code, int step) {
       if (tid == 0) {
         tl_label L;

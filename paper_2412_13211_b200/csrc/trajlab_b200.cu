@@ -300,29 +300,42 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   const int n = sp.n_env, sms = sm_count();
   const char* force = getenv("TL_RESET_EPW");  // A/B measurement only
   const int epw = force ? atoi(force) : ((int64_t)n <= (int64_t)sms * 8 ? 1 : 8);
-  const int smem = 2 * epw * kRowWords * 4;
+  // large batches: streamed seeding, one shared-memory row per episode
+  const bool stream_seed = epw >= 8 && getenv("TL_RESET_ROWS2") == nullptr;
+  const int smem = (stream_seed ? 1 : 2) * epw * kRowWords * 4;
   switch (epw) {
-    case 1: k_fuzz_reset<1><<<n, 32, smem, S(stream)>>>(sp); break;
+    case 1: k_fuzz_reset<1, false><<<n, 32, smem, S(stream)>>>(sp); break;
     case 2:
-      set_max_smem(k_fuzz_reset<2>, smem);
-      k_fuzz_reset<2><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
+      set_max_smem(k_fuzz_reset<2, false>, smem);
+      k_fuzz_reset<2, false><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
       break;
     case 4:
-      set_max_smem(k_fuzz_reset<4>, smem);
-      k_fuzz_reset<4><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
+      set_max_smem(k_fuzz_reset<4, false>, smem);
+      k_fuzz_reset<4, false><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
       break;
     case 8:
-      set_max_smem(k_fuzz_reset<8>, smem);
-      k_fuzz_reset<8><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
+      if (stream_seed) {
+        set_max_smem(k_fuzz_reset<8, true>, smem);
+        k_fuzz_reset<8, true><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
+      } else {
+        set_max_smem(k_fuzz_reset<8, false>, smem);
+        k_fuzz_reset<8, false><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
+      }
       break;
-    default:
-      set_max_smem(k_fuzz_reset<16>, 2 * 16 * kRowWords * 4);
-      k_fuzz_reset<16><<<(n + 15) / 16, 32, 2 * 16 * kRowWords * 4, S(stream)>>>(sp);
+    default: {
+      const int sm16 = (stream_seed ? 1 : 2) * 16 * kRowWords * 4;
+      if (stream_seed) {
+        set_max_smem(k_fuzz_reset<16, true>, sm16);
+        k_fuzz_reset<16, true><<<(n + 15) / 16, 32, sm16, S(stream)>>>(sp);
+      } else {
+        set_max_smem(k_fuzz_reset<16, false>, sm16);
+        k_fuzz_reset<16, false><<<(n + 15) / 16, 32, sm16, S(stream)>>>(sp);
+      }
+    }
   }
 }
 
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
-  const int rows_smem = 32 * kRowWords * 4;
   // realize + label: one 3-warp CTA per episode (tl_synth_cta.cuh)
   const bool small = sp.out.dof <= 7;
   const int smem = small ? (int)sizeof(CtaSmem<7>) : (int)sizeof(CtaSmem<16>);
@@ -335,8 +348,7 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   if (fuzz) {
     launch_fuzz_reset(sp, stream);
   } else if (!fuzz) {
-    set_max_smem(k_seed_states, rows_smem);
-    k_seed_states<<<(sp.n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
+    k_seed_states<<<(sp.n_env + 127) / 128, 128, 0, S(stream)>>>(sp);
   }
   const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
   if (getenv("TL_DEBUG"))
@@ -506,9 +518,7 @@ int tl_env_reset(void* state, int32_t n_env, int32_t dof, const tl_script* scrip
   sp.scripts = const_cast<tl_script*>(scripts);
   sp.states = ep.mt;
   sp.n_env = n_env;
-  const int rows_smem = 32 * kRowWords * 4;
-  set_max_smem(k_seed_states, rows_smem);
-  k_seed_states<<<(n_env + 31) / 32, 32, rows_smem, S(stream)>>>(sp);
+  k_seed_states<<<(n_env + 127) / 128, 128, 0, S(stream)>>>(sp);
   ep.scripts = scripts;
   ep.obs = obs;
   ep.obs_stride = obs_stride;
