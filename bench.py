@@ -348,40 +348,84 @@ def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
             "timing": "CUDA events around the whole pipeline (incl. host glue), max over ranks"}
 
 
-def c3_run(dev, stream, world, n_env=4096, reps=10):
+def fuzz_step_graph(dev, stream, n_env, kind, cfg):
+    """One fused fuzz step (tl_fuzz_ev: reset + realize + labels + ordered
+    event lists) on preallocated buffers, captured as a CUDA graph.  Returns
+    (graph, seeds_buf, workspace)."""
+    import ctypes
+    import torch
+    from paper_2412_13211_b200 import _lib as L
+    from paper_2412_13211_b200 import core
+    from paper_2412_13211_b200.thresholds import Thresholds
+    lib = L.lib()
+    cap = core.fuzz_capacity(cfg)
+    ws = core.SynthWorkspace(n_env, cap)
+    cs = core.synth_csets(Thresholds()).to_device(dev)
+    th_c = core.thresholds_c(Thresholds())
+    cfg_c = L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0, cfg.edge_density,
+                        cfg.success_prob)
+    seeds_buf = torch.zeros(n_env, dtype=torch.int64, device=dev)
+    ev_cap = 4 * n_env * cap
+    bufs = dict(ev_off=torch.empty(n_env + 1, dtype=torch.int64, device=dev),
+                ev_kind=torch.empty(ev_cap, dtype=torch.uint8, device=dev),
+                ev_t=torch.empty(ev_cap, dtype=torch.int32, device=dev))
+    rb_c = ws.records().c()
+
+    def body(s):
+        L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), n_env, kind, ctypes.byref(cfg_c),
+                               ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
+                               None, None, None, L.ptr(ws.step_mask), L.ptr(ws.labels),
+                               L.ptr(bufs["ev_off"]), L.ptr(bufs["ev_kind"]), L.ptr(bufs["ev_t"]),
+                               ev_cap, L.ptr(ws.scratch), ctypes.c_void_p(s.cuda_stream)),
+                "tl_fuzz_ev")
+    body(stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        body(torch.cuda.current_stream())
+    ws._keep = (cs, th_c, cfg_c, bufs, rb_c)
+    return g, seeds_buf, ws
+
+
+def c3_run(dev, stream, world, flush, n_env=4096, reps=20):
     """C3: Open and Close (fridge / drawer 50/50 via choice,
-    synth.py:374-376), 4096 envs per GPU each, fuzz(seed, kind) for seeds
-    [r*4096, (r+1)*4096), default FuzzConfig; generation + labels + event
-    lists (tl_fuzz_ev), device-timed per batch, max over ranks."""
+    synth.py:374-376), 4096 envs per GPU each, fuzz(seed, kind) with fresh
+    rank-disjoint seeds every batch, default FuzzConfig; generation + labels +
+    ordered event lists (tl_fuzz_ev, one CUDA graph per batch), device-timed
+    per batch with L2 flushed between batches, max over ranks."""
     import torch
     import paper_2412_13211_b200 as P
-    from paper_2412_13211_b200 import core
     rank = torch.distributed.get_rank() if world > 1 else 0
     cfg = P.FuzzConfig()
-    cs = core.synth_csets(P.Thresholds()).to_device(dev)
-    seeds = torch.arange(rank * n_env, (rank + 1) * n_env, dtype=torch.int64, device=dev)
     out = {}
     for name, kind in (("open", 2), ("close", 3)):
+        g, seeds_buf, ws = fuzz_step_graph(dev, stream, n_env, kind, cfg)
         ms, recs = [], 0
         for k in range(reps + 2):
+            seeds_buf.copy_(torch.arange(n_env, dtype=torch.int64, device=dev)
+                            + (k * world + rank) * n_env)
+            flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            sb = core.fuzz_batch(seeds, kind, cfg, P.Thresholds(), cs, events=True)
+            g.replay()
             b.record(stream)
             torch.cuda.synchronize()
             if k >= 2:
                 ms.append(a.elapsed_time(b))
-                recs = int(sb.records.n_rec.sum())
+                recs += int(ws.n_rec.sum())
         t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t = float(t.item()) / 1e3
-        lab = sb.labels.cpu().numpy().reshape(-1).view(L_LABEL_DTYPE())
+        recs /= reps
+        lab = ws.labels.cpu().numpy().reshape(-1).view(L_LABEL_DTYPE())
         out[name] = {"ms": 1e3 * t, "env_steps_per_s": recs * world / t,
                      "labelled_trajectories_per_s": n_env * world / t,
                      "mean_steps": recs / n_env, "failed": int((lab["status"] != 0).sum())}
+        del g, ws
     out["workload"] = ("C3: fuzz(seed, Open|Close), 4096 envs/GPU each, default FuzzConfig, "
-                       "generation + labels + ordered event lists (tl_fuzz_ev)")
+                       "fresh seeds per batch, generation + labels + ordered event lists "
+                       "(tl_fuzz_ev, CUDA graph), L2 flushed between batches")
     return out
 
 
@@ -686,7 +730,7 @@ def main():
         # ---- sizing run: k_label over 2^19 x 200-step episodes
         sizing = label_sizing_run(L, core, lib, dev, stream, flush)
         env_api = env_api_run(dev, stream)
-        c3 = c3_run(dev, stream, world)
+        c3 = c3_run(dev, stream, world, flush)
         c5 = c5_run(dev, stream, world)
         c4 = c4_run(dev, stream, world)
         lbf = label_batch_files_run() if rank == 0 else None
