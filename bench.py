@@ -383,7 +383,7 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         body(torch.cuda.current_stream())
-    ws._keep = (cs, th_c, cfg_c, bufs, rb_c)
+    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf)  # the graph reads these
     return g, seeds_buf, ws
 
 
@@ -466,43 +466,48 @@ def label_batch_files_run(n_files=1000):
             "reference_note": "the reference takes 0.83 s for this (BASELINE.md C8, 1 worker)"}
 
 
-def c4_run(dev, stream, world, n_chain=4096, reps=3):
+def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
     """C4: SetTable chains, 4096 per GPU; chain c runs Open,
     Pick, Place, Close twice with seeds 8c + k (k = 0..7); slot success =
     success_once; progressive_completion over the 16-slot settable plan
-    (alive counts all-reduced over ranks)."""
+    (alive counts all-reduced over ranks).  One fused fuzz graph per subtask
+    (both repetitions, 8192 episodes), then tl_chain_progress."""
     import torch
     import paper_2412_13211_b200 as P
-    from paper_2412_13211_b200 import _lib as L, core
+    from paper_2412_13211_b200 import _lib as L
     from paper_2412_13211_b200.analytics import BUILTIN_PLANS
     rank = torch.distributed.get_rank() if world > 1 else 0
     plan = BUILTIN_PLANS["settable"]
     c0 = rank * n_chain
     cfg = P.FuzzConfig()
-    cs = core.synth_csets(P.Thresholds()).to_device(dev)
     order = {"Open": 0, "Pick": 1, "Place": 2, "Close": 3}   # k within a repetition
     sub_idx = {"Pick": 0, "Place": 1, "Open": 2, "Close": 3}
     chains = torch.arange(c0, c0 + n_chain, dtype=torch.int64, device=dev)
-    # slot -> (subtask, repetition); label rows: block per (subtask, repetition)
+    subs = ["Open", "Pick", "Place", "Close"]
+    graphs = []
+    for si, sub in enumerate(subs):   # label rows [2n*si, 2n*(si+1)): rep 0 then rep 1
+        g, seeds_buf, ws = fuzz_step_graph(dev, stream, 2 * n_chain, sub_idx[sub], cfg)
+        seeds_buf.copy_(torch.cat([8 * chains + 4 * rep + order[sub] for rep in (0, 1)]))
+        graphs.append((g, ws))
     slot_label = torch.full((n_chain, len(plan)), -1, dtype=torch.int64, device=dev)
-    blocks = []
     for j, slot in enumerate(plan.slots):
         if slot.auto_success:
             continue
         rep = 0 if j < 8 else 1
-        blocks.append((j, slot.subtask, rep))
-    seeds_by_block = [(8 * chains + 4 * rep + order[sub]) for (_, sub, rep) in blocks]
-    for bi, (j, _, _) in enumerate(blocks):
-        slot_label[:, j] = bi * n_chain + torch.arange(n_chain, device=dev)
+        slot_label[:, j] = (2 * subs.index(slot.subtask) + rep) * n_chain + \
+            torch.arange(n_chain, device=dev)
+    lab = torch.empty((4 * 2 * n_chain, 24), dtype=torch.uint8, device=dev)
     alive = torch.empty(len(plan), dtype=torch.int64, device=dev)
     ms = []
     for k in range(reps + 1):
+        if flush is not None:
+            flush.zero_()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        labs = [core.fuzz_batch(sd, sub_idx[sub], cfg, P.Thresholds(), cs).labels[:n_chain]
-                for sd, (_, sub, _) in zip(seeds_by_block, blocks)]
-        lab = torch.cat(labs)
+        for si, (g, ws) in enumerate(graphs):
+            g.replay()
+            lab[2 * n_chain * si:2 * n_chain * (si + 1)].copy_(ws.labels)
         L.check(L.lib().tl_chain_progress(L.ptr(lab), L.ptr(slot_label), n_chain, len(plan),
                                           L.ptr(alive), L.stream_ptr()), "chain")
         if world > 1:
@@ -514,7 +519,8 @@ def c4_run(dev, stream, world, n_chain=4096, reps=3):
     t = sum(ms) / len(ms) / 1e3
     curve = [100.0 * int(x) / (n_chain * world) for x in alive.cpu().tolist()]
     return {"workload": "C4: SetTable chains (settable plan, 16 slots), 4096 chains/GPU, "
-                        "8 fuzz episodes per chain (seeds 8c+k), progressive_completion",
+                        "8 fuzz episodes per chain (seeds 8c+k), one fused fuzz graph per "
+                        "subtask, progressive_completion",
             "chains_per_gpu": n_chain, "n_gpus": world, "ms": 1e3 * t,
             "chains_per_s": n_chain * world / t,
             "labelled_trajectories_per_s": 8 * n_chain * world / t,
@@ -732,7 +738,7 @@ def main():
         env_api = env_api_run(dev, stream)
         c3 = c3_run(dev, stream, world, flush)
         c5 = c5_run(dev, stream, world)
-        c4 = c4_run(dev, stream, world)
+        c4 = c4_run(dev, stream, world, flush)
         lbf = label_batch_files_run() if rank == 0 else None
     clk = clocks.summary()
 
