@@ -244,12 +244,25 @@ __device__ __forceinline__ void sig_set(Sig& z, int kind, int idx) {
   }
 }
 
+// local kind k of the subtask's alphabet (kAlpha order) -> signature field
 __device__ __forceinline__ void sig_from_state(Sig& z, int subtask, const LState& S) {
   sig_clear(z);
   z.size = S.size;
-#pragma unroll
-  for (int k = 0; k < 7; k++)
-    if (k < alphabet_size(subtask)) sig_set(z, kAlpha[subtask][k], S.last[k]);
+  const int* l = S.last;
+  switch (subtask) {
+    case TL_PICK:  // Contact, Grasped, Dropped, Success, ExcessiveCollisions
+      z.c = l[0]; z.g = l[1]; z.d = l[2]; z.s = l[3]; z.x = l[4];
+      break;
+    case TL_PLACE:  // Grasped, ObjAtGoal, RAG, ROG, ObjLeftGoal, Success, X
+      z.g = l[0]; z.oag = l[1]; z.rag = l[2]; z.rog = l[3]; z.olg = l[4]; z.s = l[5]; z.x = l[6];
+      break;
+    case TL_OPEN:  // Contact, Opened, SlightlyOpened, Closed, Success, X
+      z.c = l[0]; z.opened = l[1]; z.so = l[2]; z.closed = l[3]; z.s = l[4]; z.x = l[5];
+      break;
+    default:  // Close: Contact, Closed, SlightlyClosed, Open, Success, X
+      z.c = l[0]; z.closed = l[1]; z.sc = l[2]; z.open = l[3]; z.s = l[4]; z.x = l[5];
+      break;
+  }
   z.s1 = z.size == 3 && z.c == 0 && z.g == 1 && z.s == 2;
 }
 
