@@ -130,6 +130,33 @@ __device__ __forceinline__ void twist_phase_db(const uint32_t* od, uint32_t* nw,
   __syncthreads();
 }
 
+// The same on warps 1-2 only (named barrier 1, 64 threads; phases have <= 56
+// groups), so warp 0 can plan the episode meanwhile.
+template <int DOFMAX, int G0, int G1>
+__device__ __forceinline__ void twist_phase_db64(const uint32_t* od, uint32_t* nw, uint32_t* ring,
+                                                 uint32_t base) {
+  static_assert(G1 - G0 <= 64, "one group per thread of warps 1-2");
+  const int g = G0 + (int)threadIdx.x - 32;
+  if (g < G1) {
+    const uint4 cur = reinterpret_cast<const uint4*>(od)[g];
+    const int i = 4 * g;
+    const uint32_t nxt = i + 4 == kMtN ? nw[0] : od[i + 4];
+    auto src = [&](int k) {
+      const int ii = i + k;
+      return ii < kMtN - kMtM ? od[ii + kMtM] : nw[ii - (kMtN - kMtM)];
+    };
+    uint4 nv;
+    nv.x = mt_mix(cur.x, cur.y, src(0));
+    nv.y = mt_mix(cur.y, cur.z, src(1));
+    nv.z = mt_mix(cur.z, cur.w, src(2));
+    nv.w = mt_mix(cur.w, nxt, src(3));
+    reinterpret_cast<uint4*>(nw)[g] = nv;
+    const uint4 tv = make_uint4(mt_temper(nv.x), mt_temper(nv.y), mt_temper(nv.z), mt_temper(nv.w));
+    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX>::kMask) >> 2] = tv;
+  }
+  asm volatile("bar.sync 1, 64;\n" ::: "memory");
+}
+
 template <int DOFMAX>
 __device__ __forceinline__ void mt_twist_block_db(const uint32_t* od, uint32_t* nw, uint32_t* ring,
                                                   uint32_t base) {
@@ -355,6 +382,17 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         S.gap[i] = p.step_gap[sc.step_off + s_base + i];
       }
       __syncthreads();
+      if (first_window && warp > 0) {
+        // block 0 of the realize stream is always consumed (record 0 draws):
+        // warps 1-2 regenerate it while thread 0 plans
+        twist_phase_db64<DOFMAX, 0, 56>(S.mt[0], S.mt[1], S.wb, 0);
+        twist_phase_db64<DOFMAX, 56, 112>(S.mt[0], S.mt[1], S.wb, 0);
+        twist_phase_db64<DOFMAX, 112, 156>(S.mt[0], S.mt[1], S.wb, 0);
+      }
+      if (first_window) {
+        mt_cur = 1;
+        produced = kMtN;
+      }
       if (tid == 0) {  // plan: record/word layout + deterministic state
         PlanSt q = pcarry;
         int32_t w = w_carry, r = tau_prev;
