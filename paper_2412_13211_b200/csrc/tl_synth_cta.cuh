@@ -21,30 +21,36 @@
 
 namespace tl {
 
-constexpr int kWave = 64;                  // records per wave (warps 1-2)
-constexpr int kCtaThreads = kWave + 32;    // + warp 0 (cum chain)
+// W = records per wave = emission threads (warps 1..W/32); warp 0 runs the
+// cum chain.  W = 64 for long episodes; W = 32 (a 2-warp CTA, a quarter of
+// the ring, ~1.5x the CTAs per SM) when every episode fits one or two waves.
+constexpr int kWave = 64;
+template <int W>
+__host__ __device__ constexpr int cta_threads() { return W + 32; }
 
-template <int DOFMAX>
+template <int DOFMAX, int W = kWave>
 struct CtaCfg {
-  static constexpr int kRing = DOFMAX <= 7 ? 4096 : 8192;  // >= 64*(4+2*(2*DOFMAX+5)) + 623
+  // >= W*(4+2*(2*DOFMAX+5)) + 623 words: a wave's draws plus a block's lookahead
+  static constexpr int kRing = W == 64 ? (DOFMAX <= 7 ? 4096 : 8192) : (DOFMAX <= 7 ? 2048 : 4096);
+  static_assert(kRing >= W * (4 + 2 * (2 * DOFMAX + 5)) + 623, "ring too small");
   static constexpr uint32_t kMask = kRing - 1;
 };
 
-template <int DOFMAX>
+template <int DOFMAX, int WAVE = kWave>
 struct CtaSmem {
   uint32_t mt[2][kMtN];  // double-buffered MT state (current block, next block)
-  uint32_t wb[CtaCfg<DOFMAX>::kRing];
+  uint32_t wb[CtaCfg<DOFMAX, WAVE>::kRing];
   int32_t gap[kMaxSteps];
   int32_t tau[kMaxSteps];
   int32_t W[kMaxSteps + 1];
   int32_t hw[kMaxSteps + 1];
   StepSt st[kMaxSteps + 1];
   double dist_after[kMaxSteps];
-  double radv[kWave];
-  float cum32[kWave];
-  uint32_t ind[kWave];      // indicator bits without the cum patch
-  uint32_t eerr[kWave];
-  LState part[kWave / 32];
+  double radv[WAVE];
+  float cum32[WAVE];
+  uint32_t ind[WAVE];       // indicator bits without the cum patch
+  uint32_t eerr[WAVE];
+  LState part[WAVE / 32];
   uint8_t kind[kMaxSteps];
   uint8_t sflag[kMaxSteps];
   int32_t misc[16];
@@ -61,54 +67,16 @@ struct CtaSmem {
 // Word i reads words i+1 and i+397 (old, i < 227) or i-227 (new), i.e. a
 // group depends on groups 56-57 earlier, so three phases of <= 56 groups
 // (0..55 | 56..111 | 112..155) are each internally independent: one group
-// per thread (64 threads), 128-bit shared-memory loads/stores, every phase
-// loading before it stores (a group's i+1 neighbour is the next group's
-// first word) -> 6 barriers per 624-word block.
-template <int DOFMAX, int G0, int G1>
-__device__ __forceinline__ void twist_phase4(uint32_t* mt, uint32_t* ring, uint32_t base) {
-  static_assert(G1 - G0 <= kCtaThreads, "one group per thread");
-  const int g = G0 + threadIdx.x;
-  const bool ok = g < G1;
-  uint4 nv = make_uint4(0, 0, 0, 0);
-  if (ok) {
-    const uint4 cur = reinterpret_cast<const uint4*>(mt)[g];
-    const int i = 4 * g;
-    const uint32_t nxt = mt[i + 4 == kMtN ? 0 : i + 4];
-    auto src = [&](int k) {
-      const int ii = i + k;
-      return mt[ii < kMtN - kMtM ? ii + kMtM : ii - (kMtN - kMtM)];
-    };
-    const uint32_t s0 = src(0), s1 = src(1), s2 = src(2), s3 = src(3);
-    nv.x = mt_mix(cur.x, cur.y, s0);
-    nv.y = mt_mix(cur.y, cur.z, s1);
-    nv.z = mt_mix(cur.z, cur.w, s2);
-    nv.w = mt_mix(cur.w, nxt, s3);
-  }
-  __syncthreads();
-  if (ok) {
-    reinterpret_cast<uint4*>(mt)[g] = nv;
-    const uint4 tv = make_uint4(mt_temper(nv.x), mt_temper(nv.y), mt_temper(nv.z), mt_temper(nv.w));
-    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX>::kMask) >> 2] = tv;
-  }
-  __syncthreads();
-}
-
-template <int DOFMAX>
-__device__ __forceinline__ void mt_twist_block(uint32_t* mt, uint32_t* ring, uint32_t base) {
-  twist_phase4<DOFMAX, 0, 56>(mt, ring, base);
-  twist_phase4<DOFMAX, 56, 112>(mt, ring, base);
-  twist_phase4<DOFMAX, 112, 156>(mt, ring, base);
-}
-
+// per thread, 128-bit shared-memory accesses.
 // Double-buffered form: the new block is written to `nw` while every old
 // word stays readable in `od`, so a phase needs no barrier between its loads
 // and its stores (no write-after-read hazard): 3 barriers per 624-word block.
 // Word i reads od[i], od[i+1] (nw[0] for i = 623) and od[i+397] (i < 227) or
 // nw[i-227] (i >= 227, written by an earlier phase).
-template <int DOFMAX, int G0, int G1>
+template <int DOFMAX, int W, int G0, int G1>
 __device__ __forceinline__ void twist_phase_db(const uint32_t* od, uint32_t* nw, uint32_t* ring,
                                                uint32_t base) {
-  static_assert(G1 - G0 <= kCtaThreads, "one group per thread");
+  static_assert(G1 - G0 <= cta_threads<W>(), "one group per thread");
   const int g = G0 + threadIdx.x;
   if (g < G1) {
     const uint4 cur = reinterpret_cast<const uint4*>(od)[g];
@@ -125,19 +93,18 @@ __device__ __forceinline__ void twist_phase_db(const uint32_t* od, uint32_t* nw,
     nv.w = mt_mix(cur.w, nxt, src(3));
     reinterpret_cast<uint4*>(nw)[g] = nv;
     const uint4 tv = make_uint4(mt_temper(nv.x), mt_temper(nv.y), mt_temper(nv.z), mt_temper(nv.w));
-    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX>::kMask) >> 2] = tv;
+    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX, W>::kMask) >> 2] = tv;
   }
   __syncthreads();
 }
 
-// The same on warps 1-2 only (named barrier 1, 64 threads; phases have <= 56
-// groups), so warp 0 can plan the episode meanwhile.
-template <int DOFMAX, int G0, int G1>
-__device__ __forceinline__ void twist_phase_db64(const uint32_t* od, uint32_t* nw, uint32_t* ring,
-                                                 uint32_t base) {
-  static_assert(G1 - G0 <= 64, "one group per thread of warps 1-2");
-  const int g = G0 + (int)threadIdx.x - 32;
-  if (g < G1) {
+// The same on the emission warps only (named barrier 1, W threads; W = 32
+// takes two groups per thread), so warp 0 can plan the episode meanwhile.
+template <int DOFMAX, int W, int G0, int G1>
+__device__ __forceinline__ void twist_phase_dbe(const uint32_t* od, uint32_t* nw, uint32_t* ring,
+                                                uint32_t base) {
+#pragma unroll
+  for (int g = G0 + (int)threadIdx.x - 32; g < G1; g += W) {
     const uint4 cur = reinterpret_cast<const uint4*>(od)[g];
     const int i = 4 * g;
     const uint32_t nxt = i + 4 == kMtN ? nw[0] : od[i + 4];
@@ -152,19 +119,20 @@ __device__ __forceinline__ void twist_phase_db64(const uint32_t* od, uint32_t* n
     nv.w = mt_mix(cur.w, nxt, src(3));
     reinterpret_cast<uint4*>(nw)[g] = nv;
     const uint4 tv = make_uint4(mt_temper(nv.x), mt_temper(nv.y), mt_temper(nv.z), mt_temper(nv.w));
-    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX>::kMask) >> 2] = tv;
+    reinterpret_cast<uint4*>(ring)[((base + 4u * g) & CtaCfg<DOFMAX, W>::kMask) >> 2] = tv;
   }
-  asm volatile("bar.sync 1, 64;\n" ::: "memory");
+  asm volatile("bar.sync 1, %0;\n" ::"n"(W) : "memory");
 }
 
-template <int DOFMAX>
+template <int DOFMAX, int W>
 __device__ __forceinline__ void mt_twist_block_db(const uint32_t* od, uint32_t* nw, uint32_t* ring,
                                                   uint32_t base) {
-  twist_phase_db<DOFMAX, 0, 56>(od, nw, ring, base);
-  twist_phase_db<DOFMAX, 56, 112>(od, nw, ring, base);
-  twist_phase_db<DOFMAX, 112, 156>(od, nw, ring, base);
+  twist_phase_db<DOFMAX, W, 0, 56>(od, nw, ring, base);
+  twist_phase_db<DOFMAX, W, 56, 112>(od, nw, ring, base);
+  twist_phase_db<DOFMAX, W, 112, 156>(od, nw, ring, base);
 }
 
+template <int W>
 __device__ __forceinline__ int block_max(int v, int32_t* red) {
   const int warp = threadIdx.x >> 5;
   v = __reduce_max_sync(kFull, v);
@@ -172,7 +140,7 @@ __device__ __forceinline__ int block_max(int v, int32_t* red) {
   __syncthreads();
   int m = red[0];
 #pragma unroll
-  for (int w = 1; w < kCtaThreads / 32; w++) m = max(m, red[w]);
+  for (int w = 1; w < cta_threads<W>() / 32; w++) m = max(m, red[w]);
   return m;  // red is rewritten only after later barriers of the wave
 }
 
@@ -249,12 +217,13 @@ __device__ void ev_emit_all(const SynthParams& p) {
   }
 }
 
-template <bool FUZZ, int DOFMAX>
-__global__ void __launch_bounds__(kCtaThreads, 7)
+template <bool FUZZ, int DOFMAX, int W>
+__global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     k_synth_cta(SynthParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  CtaSmem<DOFMAX>& S = *reinterpret_cast<CtaSmem<DOFMAX>*>(smem_raw);
-  constexpr uint32_t kMask = CtaCfg<DOFMAX>::kMask;
+  CtaSmem<DOFMAX, W>& S = *reinterpret_cast<CtaSmem<DOFMAX, W>*>(smem_raw);
+  constexpr uint32_t kMask = CtaCfg<DOFMAX, W>::kMask;
+  constexpr int kCtaThreads = cta_threads<W>();
   const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
   const int dof = p.out.dof;
   float* __restrict__ P = reinterpret_cast<float*>(p.out.planes);
@@ -385,9 +354,9 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
       if (first_window && warp > 0) {
         // block 0 of the realize stream is always consumed (record 0 draws):
         // warps 1-2 regenerate it while thread 0 plans
-        twist_phase_db64<DOFMAX, 0, 56>(S.mt[0], S.mt[1], S.wb, 0);
-        twist_phase_db64<DOFMAX, 56, 112>(S.mt[0], S.mt[1], S.wb, 0);
-        twist_phase_db64<DOFMAX, 112, 156>(S.mt[0], S.mt[1], S.wb, 0);
+        twist_phase_dbe<DOFMAX, W, 0, 56>(S.mt[0], S.mt[1], S.wb, 0);
+        twist_phase_dbe<DOFMAX, W, 56, 112>(S.mt[0], S.mt[1], S.wb, 0);
+        twist_phase_dbe<DOFMAX, W, 112, 156>(S.mt[0], S.mt[1], S.wb, 0);
       }
       if (first_window) {
         mt_cur = 1;
@@ -441,7 +410,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
       int seg_hint = 0;
       const bool emitter = warp > 0;
       const int et = tid - 32;  // record slot of an emission thread
-      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += kWave) {
+      for (int r0 = r_begin; r0 < r_end && !err_code; r0 += W) {
         const int r = r0 + et;
         const bool valid = emitter && r < r_end;
         int o = 0, adv = 0, app = 0, emit = 0, sidx = 0, ev = -1, s = 0;
@@ -470,12 +439,12 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         }
         if (et == 0) S.misc[12] = s;
         const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
-        const int need_max = block_max(need, S.red);  // also publishes misc[12]
+        const int need_max = block_max<W>(need, S.red);  // also publishes misc[12]
         seg_hint = S.misc[12];
         const int wbase = 20 + 8 * min(wave_no, 12);  // profiling build only
         if (tid == 0 && e == 0) TL_STAMP(wbase);
         while ((int)produced < need_max) {
-          mt_twist_block_db<DOFMAX>(S.mt[mt_cur], S.mt[mt_cur ^ 1], S.wb, produced);
+          mt_twist_block_db<DOFMAX, W>(S.mt[mt_cur], S.mt[mt_cur ^ 1], S.wb, produced);
           mt_cur ^= 1;
           produced += kMtN;
         }
@@ -514,7 +483,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         // an erroneous wave's emission only writes inside the failed episode's
         // own record slot, and nothing of it is folded
         if (my_err) atomicMin(&S.misc[13], ((s_base + s) << 8) | my_err);
-        const int cnt = min(kWave, r_end - r0);
+        const int cnt = min(W, r_end - r0);
         if (!emitter) {
           // cum_robot_force: serial f64 recurrence (synth.py:192-196, :210-213),
           // overlapped with the emission below.  Record 0 never draws; every
@@ -651,7 +620,7 @@ __global__ void __launch_bounds__(kCtaThreads, 7)
         __syncthreads();
         if (warp == 0) {
 #pragma unroll
-          for (int w = 0; w < kWave / 32; w++) {
+          for (int w = 0; w < W / 32; w++) {
             const LState& q = S.part[w];
 #pragma unroll
             for (int k = 0; k < 7; k++)

@@ -335,15 +335,29 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   }
 }
 
+typedef void (*SynthKernel)(SynthParams);
+static SynthKernel synth_kernel(int w, bool fuzz, bool small) {
+  if (w == 32)
+    return fuzz ? (small ? k_synth_cta<true, 7, 32> : k_synth_cta<true, 16, 32>)
+                : (small ? k_synth_cta<false, 7, 32> : k_synth_cta<false, 16, 32>);
+  return fuzz ? (small ? k_synth_cta<true, 7, 64> : k_synth_cta<true, 16, 64>)
+              : (small ? k_synth_cta<false, 7, 64> : k_synth_cta<false, 16, 64>);
+}
+
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
-  // realize + label: one 3-warp CTA per episode (tl_synth_cta.cuh)
+  // realize + label: one CTA per episode (tl_synth_cta.cuh); 2-warp CTAs
+  // (32-record waves) when no episode can exceed 64 records
   const bool small = sp.out.dof <= 7;
-  const int smem = small ? (int)sizeof(CtaSmem<7>) : (int)sizeof(CtaSmem<16>);
-  void (*k)(SynthParams) = fuzz ? (small ? k_synth_cta<true, 7> : k_synth_cta<true, 16>)
-                                : (small ? k_synth_cta<false, 7> : k_synth_cta<false, 16>);
+  const char* fw = getenv("TL_SYNTH_WAVE");  // A/B measurement only
+  const int W = fw ? (atoi(fw) == 32 ? 32 : 64)
+                   : (sp.cap_per_env > 0 && sp.cap_per_env <= 64 ? 32 : 64);
+  const int threads = W + 32;
+  const int smem = W == 32 ? (small ? (int)sizeof(CtaSmem<7, 32>) : (int)sizeof(CtaSmem<16, 32>))
+                           : (small ? (int)sizeof(CtaSmem<7, 64>) : (int)sizeof(CtaSmem<16, 64>));
+  SynthKernel k = synth_kernel(W, fuzz, small);
   set_max_smem(k, smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCtaThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
   if (per_sm < 1) per_sm = 1;
   if (fuzz) {
     launch_fuzz_reset(sp, stream);
@@ -352,9 +366,9 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   }
   const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
   if (getenv("TL_DEBUG"))
-    fprintf(stderr, "k_synth_cta: %d CTAs/SM (smem %d B, %d threads), grid %d\n", per_sm, smem,
-            kCtaThreads, grid);
-  k<<<grid, kCtaThreads, smem, S(stream)>>>(sp);
+    fprintf(stderr, "k_synth_cta<W=%d>: %d CTAs/SM (smem %d B, %d threads), grid %d\n", W, per_sm,
+            smem, threads, grid);
+  k<<<grid, threads, smem, S(stream)>>>(sp);
   return check_launch();
 }
 
