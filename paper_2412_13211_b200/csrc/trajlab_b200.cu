@@ -292,26 +292,37 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
 }
 
 // k_fuzz_reset with EPW episodes per warp (2*EPW seeding lanes): one
-// episode per warp while that keeps <= 8 warps per SM, else 8 per warp --
-// the seeding chains are latency-bound and more warps contend for issue,
-// while the sampler is branchy code that diverges across episodes
-// (measured: scripts/reset_epw_ab.sh, 1k-250k episodes)
+// episode per warp while that keeps <= 8 warps per SM, 4 up to 64 episodes
+// per SM, else 8 -- the seeding chains are latency-bound and more warps
+// contend for issue, while the sampler is branchy code that diverges across
+// episodes (measured: scripts/reset_epw_ab.sh, scripts/reset_epw_ab2.sh)
 static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   const int n = sp.n_env, sms = sm_count();
   const char* force = getenv("TL_RESET_EPW");  // A/B measurement only
-  const int epw = force ? atoi(force) : ((int64_t)n <= (int64_t)sms * 8 ? 1 : 8);
+  const int epw = force ? atoi(force)
+                        : (int64_t)n <= (int64_t)sms * 8 ? 1 : (int64_t)n <= (int64_t)sms * 64 ? 4 : 8;
   // large batches: streamed seeding, one shared-memory row per episode
-  const bool stream_seed = epw >= 8 && getenv("TL_RESET_ROWS2") == nullptr;
+  const bool stream_seed = epw >= 2 && getenv("TL_RESET_ROWS2") == nullptr;
   const int smem = (stream_seed ? 1 : 2) * epw * kRowWords * 4;
   switch (epw) {
     case 1: k_fuzz_reset<1, false><<<n, 32, smem, S(stream)>>>(sp); break;
     case 2:
-      set_max_smem(k_fuzz_reset<2, false>, smem);
-      k_fuzz_reset<2, false><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
+      if (stream_seed) {
+        set_max_smem(k_fuzz_reset<2, true>, smem);
+        k_fuzz_reset<2, true><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
+      } else {
+        set_max_smem(k_fuzz_reset<2, false>, smem);
+        k_fuzz_reset<2, false><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
+      }
       break;
     case 4:
-      set_max_smem(k_fuzz_reset<4, false>, smem);
-      k_fuzz_reset<4, false><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
+      if (stream_seed) {
+        set_max_smem(k_fuzz_reset<4, true>, smem);
+        k_fuzz_reset<4, true><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
+      } else {
+        set_max_smem(k_fuzz_reset<4, false>, smem);
+        k_fuzz_reset<4, false><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
+      }
       break;
     case 8:
       if (stream_seed) {
