@@ -557,3 +557,32 @@ def test_fuzz_extreme_seeds_vs_oracle(C, TH):
             assert nr[i] == len(recs), (kind, sd)
             p, _ = from_oracle_records(O, recs)
             assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), (kind, sd)
+
+
+@pytest.mark.parametrize("long_cfg", [False, True])
+@pytest.mark.parametrize("kind", range(4))
+def test_realize_wave_variants_identical(C, TH, kind, long_cfg, monkeypatch):
+    """The realize kernel's 2-warp (32-record waves) and 3-warp (64-record
+    waves) forms, and every reset layout (episodes per warp 1/4/8), produce
+    identical records, labels and step masks."""
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    seeds = np.arange(1200 if long_cfg else 3000) + 90210 * (kind + 1)
+    cfg = FuzzConfig(max_gap=64, max_tail=64) if long_cfg else FuzzConfig()
+    outs = []
+    for wave, epw in (("64", "1"), ("32", "4"), ("64", "8"), ("32", "8")):
+        monkeypatch.setenv("TL_SYNTH_WAVE", wave)
+        monkeypatch.setenv("TL_RESET_EPW", epw)
+        sb = C.fuzz_batch(seeds, kind, cfg, TH(), cs, events=True)
+        rs = sb.records.rec_start.cpu().numpy()
+        nr = sb.records.n_rec.cpu().numpy()
+        planes = sb.records.planes.cpu().numpy()
+        recs = np.concatenate([planes[:, rs[i]:rs[i] + nr[i]] for i in range(len(seeds))], axis=1)
+        masks = sb.step_mask.cpu().numpy()
+        m = np.concatenate([masks[rs[i]:rs[i] + nr[i]] for i in range(len(seeds))])
+        ev = sb.label_result
+        outs.append((sb.labels.cpu().numpy().tobytes(), recs.view(np.uint32).tobytes(), m.tobytes(),
+                     ev.ev_kind[:int(ev.ev_off[-1])].cpu().numpy().tobytes(),
+                     ev.ev_t[:int(ev.ev_off[-1])].cpu().numpy().tobytes()))
+    for o in outs[1:]:
+        assert o == outs[0]
