@@ -38,21 +38,24 @@ struct CtaCfg {
 
 template <int DOFMAX, int WAVE = kWave>
 struct CtaSmem {
+  // script steps planned per window (scripts are re-planned window by
+  // window); the short-episode form plans 32 at a time to fit 12 CTAs/SM
+  static constexpr int kSteps = WAVE == 32 ? 32 : kMaxSteps;
   uint32_t mt[2][kMtN];  // double-buffered MT state (current block, next block)
   uint32_t wb[CtaCfg<DOFMAX, WAVE>::kRing];
-  int32_t gap[kMaxSteps];
-  int32_t tau[kMaxSteps];
-  int32_t W[kMaxSteps + 1];
-  int32_t hw[kMaxSteps + 1];
-  StepSt st[kMaxSteps + 1];
-  double dist_after[kMaxSteps];
+  int32_t gap[kSteps];
+  int32_t tau[kSteps];
+  int32_t W[kSteps + 1];
+  int32_t hw[kSteps + 1];
+  StepSt st[kSteps + 1];
+  double dist_after[kSteps];
   double radv[WAVE];
   float cum32[WAVE];
   uint32_t ind[WAVE];       // indicator bits without the cum patch
   uint32_t eerr[WAVE];
   LState part[WAVE / 32];
-  uint8_t kind[kMaxSteps];
-  uint8_t sflag[kMaxSteps];
+  uint8_t kind[kSteps];
+  uint8_t sflag[kSteps];
   int32_t misc[16];
   int32_t red[8];
   tl_cset cs;
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     PlanSt pcarry = ps;
     bool first_window = true;
     for (;;) {
-      const int ns = min(n_steps - s_base, kMaxSteps);
+      const int ns = min(n_steps - s_base, CtaSmem<DOFMAX, W>::kSteps);
       const bool last_window = s_base + ns >= n_steps;
       for (int i = tid; i < ns; i += kCtaThreads) {
         S.kind[i] = p.step_kind[sc.step_off + s_base + i];

@@ -586,3 +586,30 @@ def test_realize_wave_variants_identical(C, TH, kind, long_cfg, monkeypatch):
                      ev.ev_t[:int(ev.ev_off[-1])].cpu().numpy().tobytes()))
     for o in outs[1:]:
         assert o == outs[0]
+
+
+@pytest.mark.parametrize("kind", range(4))
+def test_short_wave_multi_window_vs_oracle(C, TH, kind):
+    """Episodes of <= 64 records but up to 44 script steps: the 2-warp
+    realize form (32-record waves) plans them in windows of 32 steps; records
+    and labels == the oracle's fuzz."""
+    from oracle import oracle as O
+    from golden_data import from_oracle_records
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_events=40, max_gap=1, max_tail=1)
+    assert C.fuzz_capacity(cfg) <= 64          # selects the 2-warp form
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 400
+    sb = C.fuzz_batch(np.arange(n) + 777 * (kind + 1), kind, cfg, TH(), cs, want_scripts=True)
+    lab = sb.labels.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    planes = sb.records.planes.cpu().numpy()
+    rs = sb.records.rec_start.cpu().numpy()
+    ocfg = O.fuzz_cfg(max_events=40, max_gap=1, max_tail=1)
+    multi = 0
+    for i in range(n):
+        sc, recs = O.fuzz(777 * (kind + 1) + i, kind, ocfg)
+        multi += len(sc["kinds"]) > 32
+        assert lab["status"][i] == 0, (i, lab["status"][i])
+        p, _ = from_oracle_records(O, recs)
+        assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), i
+    assert multi > 10
