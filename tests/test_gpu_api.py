@@ -291,6 +291,13 @@ def test_c5_device_filter_matches_host_filter():
     n = 1500
     labels, man, names = D.fuzz_label_filter_sharded(n, spec, n_targets=9)
     lab = labels.cpu().numpy().reshape(-1).view(L.LABEL_DTYPE)
+    # the four side-stream batches == plain per-subtask fuzz batches
+    import torch
+    from paper_2412_13211_b200 import core
+    cs = core.synth_csets(P.Thresholds()).to_device(torch.device("cuda"))
+    for s in range(4):
+        ref = core.fuzz_batch(np.arange(n), s, P.FuzzConfig(), P.Thresholds(), cs).labels[:n]
+        assert np.array_equal(ref.cpu().numpy(), labels[s * n:(s + 1) * n].cpu().numpy()), s
     recs = []
     for s, kind in enumerate(SUBTASK_ORDER):
         for seed in range(n):
