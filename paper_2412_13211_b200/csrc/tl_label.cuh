@@ -680,6 +680,14 @@ __device__ __forceinline__ void record_bits_s(const K& k, float der, float cum, 
 }
 
 constexpr int kLabelWarpsMax = 8;
+#ifndef TL_LABEL_QD_SMEM
+#define TL_LABEL_QD_SMEM 1  // Pick / Place: qd planes staged in shared memory
+#endif
+// one staging buffer per block for every subtask's body: [warp][plane][lane]
+__device__ __forceinline__ float4 (*qd_stage())[32] {
+  __shared__ __align__(16) float4 buf[kLabelWarpsMax * 7][32];
+  return buf;
+}
 #ifndef TL_VEC_INL
 #define TL_VEC_INL __forceinline__  // inlined: the running state stays in registers
 #endif
@@ -715,12 +723,25 @@ __device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, in
 #pragma unroll
     for (int j = 0; j < RPL; j++) ind[j] = err[j] = 0u;
     if (tb < n) {
-      // every load of the chunk issued up front
+      // every load of the chunk issued up front; Pick / Place stage the qd
+      // planes in shared memory (cp.async: no registers held in flight),
+      // which at 64 registers lets ptxas issue the rest in one batch
+      constexpr bool kStageQd = TL_LABEL_QD_SMEM && (SUB == TL_PICK || SUB == TL_PLACE);
+      static_assert(!kStageQd || DOF <= 7, "qd staging holds 7 planes");
       float4 q[DOF], qd[DOF];
+      float4 (*sq)[32] = kStageQd ? qd_stage() + (threadIdx.x >> 5) * 7 : nullptr;
+      if (kStageQd) {
 #pragma unroll
-      for (int i = 0; i < DOF; i++) {
-        q[i] = ldf4(p + i * stride);
-        qd[i] = ldf4(p + (DOF + i) * stride);
+        for (int i = 0; i < DOF; i++) cp_async16(&sq[i][lane], p + (DOF + i) * stride);
+        cp_async_commit();
+#pragma unroll
+        for (int i = 0; i < DOF; i++) q[i] = ldf4(p + i * stride);
+      } else {
+#pragma unroll
+        for (int i = 0; i < DOF; i++) {
+          q[i] = ldf4(p + i * stride);
+          qd[i] = ldf4(p + (DOF + i) * stride);
+        }
       }
       const float4 der4 = ldf4(p + (f0 + 4) * stride), cum4 = ldf4(p + (f0 + 7) * stride);
       const float4 vx4 = ldf4(p + (f0 + 1) * stride), vy4 = ldf4(p + (f0 + 2) * stride);
@@ -740,6 +761,11 @@ __device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, in
       // Python max() of |q_i| and |qd_i| per record (predicates.py:20, :24)
       float mq[RPL], mqd[RPL];
       pymax4<DOF>(q, mq);
+      if (kStageQd) {
+        cp_async_wait<0>();
+#pragma unroll
+        for (int i = 0; i < DOF; i++) qd[i] = sq[i][lane];
+      }
       pymax4<DOF>(qd, mqd);
 #pragma unroll
       for (int j = 0; j < RPL; j++) {
