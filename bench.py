@@ -117,6 +117,21 @@ def profile_traffic():
         return None, None
 
 
+def host_info():
+    """The host the CPU baseline ran on (core count, CPU model, Python)."""
+    import platform
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model, "python": platform.python_version()}
+
+
 def cpu_baseline(seconds, n_threads=1):
     """CPU oracle (C restatement of the reference path) on a bounded sample."""
     from oracle import oracle as O
@@ -162,7 +177,7 @@ def run_reference(args, rank, world):
            "cpu_baseline": {"value": sps, "unit": "env-steps/s", "cores": cores, "kind": "port",
                             "sample": f"{args.steps} steps x {n_env} episodes, oracle/oracle.c "
                                       "(C restatement of trajlab fuzz+extract_events+classify), "
-                                      f"{cores} threads"},
+                                      f"{cores} threads", "host": host_info()},
            "e2e": {"value": sps, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -808,7 +823,8 @@ def main():
         "c4": c4,
         "label_batch_files": lbf,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
-                         "sample": cb_sample, "trajectories_per_sec": cb_eps},
+                         "sample": cb_sample, "trajectories_per_sec": cb_eps,
+                         "host": host_info()},
         "clocks": clk,
     }
     print(json.dumps(out))
