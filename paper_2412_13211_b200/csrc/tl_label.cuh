@@ -192,22 +192,20 @@ __device__ __forceinline__ void lstate_init(LState& S) {
 
 // fold one chunk's per-lane event masks into the running state
 __device__ __forceinline__ void lstate_fold(LState& S, uint32_t mask, uint32_t err) {
-  const uint32_t orm = __reduce_or_sync(kFull, mask);
-  if (orm) {  // warp-uniform: events are sparse, most chunks have none
-    const int cnt = __popc(mask);
-    const int incl = warp_incl_scan(cnt);
-    const int excl = incl - cnt;
+  const int cnt = __popc(mask);
+  const int incl = warp_incl_scan(cnt);
+  const int excl = incl - cnt;
 #pragma unroll
-    for (int k = 0; k < 7; k++) {
-      if (!((orm >> k) & 1u)) continue;
-      const unsigned bal = __ballot_sync(kFull, (mask >> k) & 1u);
+  for (int k = 0; k < 7; k++) {
+    const unsigned bal = __ballot_sync(kFull, (mask >> k) & 1u);
+    if (bal) {
       const int L = 31 - __clz(bal);
       const int exL = __shfl_sync(kFull, excl, L);
       const uint32_t mL = __shfl_sync(kFull, mask, L);
       S.last[k] = S.size + exL + __popc(mL & ((1u << k) - 1u));
     }
-    S.size += __shfl_sync(kFull, incl, 31);
   }
+  S.size += __shfl_sync(kFull, incl, 31);
   S.err_any |= __reduce_or_sync(kFull, err);
 }
 
