@@ -903,9 +903,13 @@ static_assert(kLabelWarps <= kLabelWarpsMax, "label_vec_d's per-warp state");
 #define TL_LABEL_MINB 4  // f32, arm_dof <= 7: 4 x 8 warps per SM at <= 64 registers
 #endif
 
-template <typename T, int DOFMAX>
-__global__ void __launch_bounds__(kLabelWarps * 32,
-                                  (sizeof(T) == 4 && DOFMAX == 7) ? TL_LABEL_MINB : 2)
+// PART 1: only the episodes the compile-time-dof vector bodies take (f32,
+// arm_dof 7, zero rest posture, 4-record aligned, >= 2 records); PART 2: all
+// others; PART 0: every episode.  f32 / arm_dof <= 7 batches launch PART 1
+// then PART 2, so the hot vector kernel's registers are allocated without
+// the generic bodies (which share nothing with it at run time).
+template <typename T, int DOFMAX, int PART>
+__global__ void __launch_bounds__(kLabelWarps * 32, PART == 1 ? TL_LABEL_MINB : 2)
     k_label(tl_records R, int n_env, const int32_t* __restrict__ env_cset,
             const tl_cset* __restrict__ csets, tl_rules rules,
             uint8_t* __restrict__ step_mask, uint8_t* __restrict__ step_success,
@@ -917,14 +921,16 @@ __global__ void __launch_bounds__(kLabelWarps * 32,
   const int dof = R.dof;
   const bool vec_ok = (stride & 3) == 0 && (reinterpret_cast<uintptr_t>(R.planes) & 15) == 0 &&
                       (reinterpret_cast<uintptr_t>(R.grasped) & 3) == 0;
-  for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
-    stage_cset(&s_cs[warp], &csets[env_cset[e]]);
+  auto fast_ok = [&](int ci, int64_t rs, int n) {
+    return sizeof(T) == 4 && DOFMAX == 7 && dof == 7 && !vec_generic && n >= 2 && (rs & 3) == 0 &&
+           vec_ok && rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride && csets[ci].rest_zero;
+  };
+  auto process = [&](int e, int ci, int64_t rs, int n) {
+    stage_cset(&s_cs[warp], &csets[ci]);
     const tl_cset& c = s_cs[warp];
-    const int64_t rs = R.rec_start[e];
-    const int n = R.n_rec[e];
     LState S;
     lstate_init(S);
-    if (n < 2) {  // events.py:96-97
+    if (PART != 1 && n < 2) {  // events.py:96-97
       if (lane == 0) {
         tl_label L;
         L.status = TL_ERR_TOO_SHORT; L.n_events = 0; L.err_index = -1;
@@ -935,7 +941,7 @@ __global__ void __launch_bounds__(kLabelWarps * 32,
       if (step_success) {  // predicate values are still defined per record
         // fallthrough below handles n == 1 through the generic loop
       } else {
-        continue;
+        return;
       }
     }
     const int f0 = 2 * dof;
@@ -944,24 +950,58 @@ __global__ void __launch_bounds__(kLabelWarps * 32,
     double sc_d = 0.0;
     if (c.subtask == TL_PLACE) d0 = (double)P[(f0 + 5) * stride + rs];
     if (c.subtask == TL_CLOSE && n > 0) close_cut(c, (double)P[(f0 + 8) * stride + rs], sc_ru, sc_d);
+    if (PART == 1) {  // compile-time-dof vector bodies
+      switch (c.subtask) {
+        case TL_PICK: label_vec_d<7, TL_PICK>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+        case TL_PLACE: label_vec_d<7, TL_PLACE>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+        case TL_OPEN: label_vec_d<7, TL_OPEN>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+        default: label_vec_d<7, TL_CLOSE>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
+      }
+      finish_label(c, S, d0, rules, &labels[e]);
+      return;
+    }
     // f32 episodes whose records are 16-byte aligned: 4 records per lane,
-    // 128-bit loads (k_label_vec4); otherwise one record per lane below.
+    // 128-bit loads (label_vec4); otherwise one record per lane below.
     if (sizeof(T) == 4 && c.rest_zero && (rs & 3) == 0 && vec_ok &&
         rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride) {
-      if (dof == 7 && !vec_generic) {
-        switch (c.subtask) {
-          case TL_PICK: label_vec_d<7, TL_PICK>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-          case TL_PLACE: label_vec_d<7, TL_PLACE>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-          case TL_OPEN: label_vec_d<7, TL_OPEN>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-          default: label_vec_d<7, TL_CLOSE>(R, c, rs, n, sc_ru, S, step_mask, step_success); break;
-        }
-      } else
-        label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
+      label_vec4(R, c, rs, n, sc_ru, (double)sc_d, S, step_mask, step_success);
       if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
-      continue;
+      return;
     }
     label_scalar<T, DOFMAX>(R, c, rs, n, sc_ru, sc_d, S, step_mask, step_success);
     if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
+  };
+  if (PART == 2) {
+    // 32 episodes per warp iteration: lane l tests episode base + l, the warp
+    // then labels the ones the vector kernel left (usually none)
+    for (int64_t base = ((int64_t)blockIdx.x * kLabelWarps + warp) * 32; base < n_env;
+         base += (int64_t)gridDim.x * kLabelWarps * 32) {
+      const int el = (int)base + lane;
+      int ci = 0, n = 0;
+      int64_t rs = 0;
+      bool todo_l = false;
+      if (el < n_env) {
+        ci = env_cset[el];
+        rs = R.rec_start[el];
+        n = R.n_rec[el];
+        todo_l = !fast_ok(ci, rs, n);
+      }
+      unsigned todo = __ballot_sync(kFull, todo_l);
+      while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        process((int)base + j, __shfl_sync(kFull, ci, j), __shfl_sync(kFull, rs, j),
+                __shfl_sync(kFull, n, j));
+      }
+    }
+    return;
+  }
+  for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
+    const int ci = env_cset[e];
+    const int64_t rs = R.rec_start[e];
+    const int n = R.n_rec[e];
+    if (PART == 1 && !fast_ok(ci, rs, n)) continue;
+    process(e, ci, rs, n);
   }
 }
 

@@ -222,11 +222,15 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
                                                    step_success, labels);
     }
   } else if (recs->dtype == 0) {
-    if (small) k_label<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
-    else k_label<float, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    if (small) {  // vector-body episodes, then everything else (k_label PART 1 / 2)
+      k_label<float, 7, 1><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+      k_label<float, 7, 2><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    } else {
+      k_label<float, 16, 0><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    }
   } else {
-    if (small) k_label<double, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
-    else k_label<double, 16><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    if (small) k_label<double, 7, 0><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
+    else k_label<double, 16, 0><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
   }
   return check_launch();
 }
