@@ -971,7 +971,7 @@ __global__ void __launch_bounds__(kLabelWarps * 32, PART == 1 ? TL_LABEL_MINB : 
     label_scalar<T, DOFMAX>(R, c, rs, n, sc_ru, sc_d, S, step_mask, step_success);
     if (n >= 2) finish_label(c, S, d0, rules, &labels[e]);
   };
-  if (PART == 2) {
+  if constexpr (PART == 2) {
     // 32 episodes per warp iteration: lane l tests episode base + l, the warp
     // then labels the ones the vector kernel left (usually none)
     for (int64_t base = ((int64_t)blockIdx.x * kLabelWarps + warp) * 32; base < n_env;
@@ -994,14 +994,14 @@ __global__ void __launch_bounds__(kLabelWarps * 32, PART == 1 ? TL_LABEL_MINB : 
                 __shfl_sync(kFull, n, j));
       }
     }
-    return;
-  }
-  for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
-    const int ci = env_cset[e];
-    const int64_t rs = R.rec_start[e];
-    const int n = R.n_rec[e];
-    if (PART == 1 && !fast_ok(ci, rs, n)) continue;
-    process(e, ci, rs, n);
+  } else {
+    for (int e = blockIdx.x * kLabelWarps + warp; e < n_env; e += gridDim.x * kLabelWarps) {
+      const int ci = env_cset[e];
+      const int64_t rs = R.rec_start[e];
+      const int n = R.n_rec[e];
+      if (PART == 1 && !fast_ok(ci, rs, n)) continue;
+      process(e, ci, rs, n);
+    }
   }
 }
 
