@@ -680,6 +680,9 @@ __device__ __forceinline__ void record_bits_s(const K& k, float der, float cum, 
 }
 
 constexpr int kLabelWarpsMax = 8;
+#ifndef TL_LABEL_L2PF
+#define TL_LABEL_L2PF 1
+#endif
 #ifndef TL_LABEL_QD_SMEM
 #define TL_LABEL_QD_SMEM 1  // Pick / Place: qd planes staged in shared memory
 #endif
@@ -730,6 +733,14 @@ __device__ TL_VEC_INL void label_vec_d(const tl_records& R, const tl_cset& c, in
       static_assert(!kStageQd || DOF <= 7, "qd staging holds 7 planes");
       float4 q[DOF], qd[DOF];
       float4 (*sq)[32] = kStageQd ? qd_stage() + (threadIdx.x >> 5) * 7 : nullptr;
+      // Open / Close (qd planes in registers): the next chunk's q / qd planes
+      // are prefetched toward L2 while this one is labelled
+      constexpr bool kL2Pf = TL_LABEL_L2PF && (SUB == TL_OPEN || SUB == TL_CLOSE);
+      if (kL2Pf && tb + CH < n) {
+#pragma unroll
+        for (int i = 0; i < 2 * DOF; i++)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + CH + i * stride));
+      }
       if (kStageQd) {
 #pragma unroll
         for (int i = 0; i < DOF; i++) cp_async16(&sq[i][lane], p + (DOF + i) * stride);
