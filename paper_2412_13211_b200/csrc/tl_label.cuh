@@ -5,8 +5,10 @@
 //   events.py:94-193      extract_events (edge tests in EVENT_ORDER)
 //   modes.py:24-253       last_index / _Ctx / rule tables / classify
 //
-// Mapping: one warp per episode, lane = timestep within a 32-record chunk.
-// Each lane evaluates its record's indicator bits; the previous record's
+// Mapping: one warp per episode; f32 episodes at arm_dof 7 with aligned
+// slots take the vector bodies (4 consecutive records per lane, 128-record
+// chunks, k_label<float,7,1>), everything else one record per lane (32-record
+// chunks).  Each lane evaluates its records' indicator bits; the previous record's
 // bits arrive by __shfl_up (carry across chunks); events are the per-step
 // bitmask in EVENT_ORDER bit order.  The event list itself is never stored
 // here: classification needs only |E|, the last index of each kind and d0

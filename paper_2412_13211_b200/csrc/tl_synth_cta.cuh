@@ -1,21 +1,28 @@
-// tl_synth_cta.cuh -- realize + online labelling with one 3-warp CTA per
-// episode (the latency-optimised form of k_synth).
+// tl_synth_cta.cuh -- realize + online labelling with one CTA per episode.
 //
-// Same semantics as k_synth (tl_synth.cuh; reference synth.py:100-348 +
-// events.py:94-193 + modes.py:235-253), different mapping:
-//   * MT19937 block regeneration is spread over 64 threads in three phases
-//     of 4-word groups (6 barriers per block, 128-bit shared accesses);
-//   * a wave of 64 records is emitted at once, one record per thread, from
-//     a 16 KB ring of tempered words (small enough that all episodes of a
-//     1024-env batch are resident at once: ~23 KB shared memory per CTA);
+// Semantics: reference synth.py:100-348 (_Realizer) fused with
+// events.py:94-193 (extract_events) and modes.py:235-253 (classify).
+// Mapping (W = records per wave: 64 = 3 warps, 32 = 2 warps for batches
+// whose episodes fit 64 records):
+//   * thread 0 plans the script window (exact MT word offset of every
+//     record and the deterministic per-step state); meanwhile the emission
+//     warps regenerate the episode's first MT block;
+//   * MT19937 block regeneration in three phases of 4-word groups,
+//     double-buffered (old / new block arrays): 3 barriers per block,
+//     128-bit shared accesses, tempered words into a ring;
+//   * a wave of W records is emitted at once, one record per emission
+//     thread, from the ring (4096 / 2048 words: all CTAs of a 1024-episode
+//     batch are resident at once);
 //   * the serial f64 cum_robot_force recurrence runs on warp 0, eight
 //     records per group of vector shared-memory loads, split at the
 //     ExcessiveCollisions record (before it every step draws, after it cum
-//     is constant), CONCURRENTLY with the emission of the same wave by
-//     warps 1-2 (one record per thread); the cum-dependent label bits are
-//     patched in afterwards (cum_patch_bits);
+//     is constant), CONCURRENTLY with the emission of the same wave; the
+//     cum-dependent label bits are patched in afterwards (cum_patch_bits);
 //   * each emission warp folds its 32 event masks into a partial label
-//     state, combined in order by warp 0.
+//     state, combined in order by warp 0; persistent CTAs prefetch their
+//     next episode's seeded state and script by cp.async;
+//   * tl_fuzz_ev: the ordered event lists are written by the same kernel
+//     after a warp-wide decoupled look-back over the episodes' event counts.
 #pragma once
 #include "tl_synth.cuh"
 
