@@ -199,7 +199,12 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
   const tl_rules r = rules_or_default(rules);
-  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * 16);
+  // 128 blocks (of 8 warps) per SM, grid-stride beyond: each warp labels ~7
+  // episodes of a 2^20-episode batch, and the episodes in flight stay close
+  // in memory (measured: 16/SM 84 %, 128/SM 89 %, one block per 8 episodes 78 %
+  // of HBM on the Pick sizing run)
+  const char* gm = getenv("TL_LABEL_GRID_PER_SM");  // A/B measurement only
+  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * (gm ? atoi(gm) : 128));
   const dim3 blk(kLabelWarps * 32);
   const bool small = recs->dof <= 7;
   // TL_LABEL_TMA=1 selects the shared-memory (TMA bulk copy) staged variant;
@@ -751,7 +756,12 @@ int tl_eval_predicates(const tl_records* recs, int32_t n_env, const int32_t* env
       (recs->dtype != 0 && recs->dtype != 1))
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
-  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * 16);
+  // 128 blocks (of 8 warps) per SM, grid-stride beyond: each warp labels ~7
+  // episodes of a 2^20-episode batch, and the episodes in flight stay close
+  // in memory (measured: 16/SM 84 %, 128/SM 89 %, one block per 8 episodes 78 %
+  // of HBM on the Pick sizing run)
+  const char* gm = getenv("TL_LABEL_GRID_PER_SM");  // A/B measurement only
+  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * (gm ? atoi(gm) : 128));
   const dim3 blk(kLabelWarps * 32);
   if (recs->dtype == 0) {
     if (recs->dof <= 7) k_predicates<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, a0, bits, errs, jmax);
