@@ -285,7 +285,7 @@ int tl_emit_events(const uint8_t* step_mask, const int64_t* rec_start, const int
                                   !ev_kind || !ev_t)))
     return TL_E_INVALID;
   if (n_env == 0) return TL_OK;
-  const int grid = blocks_for(n_env, kEmitWarps, sm_count() * 16);
+  const int grid = blocks_for(n_env, kEmitWarps, sm_count() * 128);  // as k_label
   k_emit<<<grid, kEmitWarps * 32, 0, S(stream)>>>(step_mask, rec_start, n_rec, labels, ev_off, n_env, ev_kind, ev_t);
   return check_launch();
 }
