@@ -908,6 +908,11 @@ typedef struct {
   uint8_t* mode_out;
   int32_t* nev_out;
   int64_t* nrec_out;
+  uint8_t* flags_out;   /* optional: bit 0 success_once, bit 1 success_at_end */
+  double* d0_out;       /* optional: initial_dist_obj_goal (NaN if absent) */
+  int64_t ev_stride;    /* optional event lists: ev_*_out[i * ev_stride + k] */
+  uint8_t* ev_kind_out;
+  int32_t* ev_t_out;
   int64_t base;
   int64_t records;
 } job_t;
@@ -933,23 +938,27 @@ static void* fuzz_job(void* arg) {
     (void)ns;
     int32_t es;
     int64_t n = or_realize(&s, seed ^ 0x5EED, J->th, recs, rcap, &es);
-    int32_t mode = -1, nev = 0;
+    int32_t mode = -1, nev = 0, so = 0, se = 0;
+    double d0 = NAN;
     if (n > 0) {
       h.art_kind = (J->kind == OR_OPEN || J->kind == OR_CLOSE) ? s.art_kind : OR_ART_NONE;
       h.art_qmin = h.art_kind == OR_ART_FRIDGE ? 0.0 : h.art_kind == OR_ART_DRAWER ? 0.0 : NAN;
       h.art_qmax = h.art_kind == OR_ART_FRIDGE ? 1.6 : h.art_kind == OR_ART_DRAWER ? 0.5 : NAN;
-      double d0;
       nev = or_extract_events(recs, n, &h, J->th, ek, et, (int32_t)(4 * rcap), &d0);
-      if (nev >= 0) {
-        int32_t so, se;
-        mode = or_classify(J->kind, ek, nev, d0, 0, NULL, 0, &so, &se);
-      }
+      if (nev >= 0) mode = or_classify(J->kind, ek, nev, d0, 0, NULL, 0, &so, &se);
       J->records += n;
     }
     int64_t i = seed - J->base;
     if (J->mode_out) J->mode_out[i] = (uint8_t)(mode < 0 ? 255 : mode);
     if (J->nev_out) J->nev_out[i] = nev;
     if (J->nrec_out) J->nrec_out[i] = n;
+    if (J->flags_out) J->flags_out[i] = (uint8_t)((mode >= 0 && so ? 1 : 0) | (mode >= 0 && se ? 2 : 0));
+    if (J->d0_out) J->d0_out[i] = d0;
+    if (J->ev_kind_out && nev > 0) {
+      const int64_t m = nev < J->ev_stride ? nev : J->ev_stride;
+      memcpy(J->ev_kind_out + i * J->ev_stride, ek, (size_t)m);
+      memcpy(J->ev_t_out + i * J->ev_stride, et, sizeof(int32_t) * (size_t)m);
+    }
   }
   free(sk);
   free(sg);
@@ -959,10 +968,12 @@ static void* fuzz_job(void* arg) {
   return NULL;
 }
 
-int64_t or_fuzz_label_batch(int64_t seed0, int64_t n, int32_t subtask,
-                            const or_fuzz_cfg* cfg, const or_thresholds* th,
-                            int32_t n_threads, uint8_t* mode_out,
-                            int32_t* n_events_out, int64_t* n_records_out) {
+int64_t or_fuzz_label_batch_ex(int64_t seed0, int64_t n, int32_t subtask,
+                               const or_fuzz_cfg* cfg, const or_thresholds* th,
+                               int32_t n_threads, uint8_t* mode_out,
+                               int32_t* n_events_out, int64_t* n_records_out,
+                               uint8_t* flags_out, double* d0_out, int64_t ev_stride,
+                               uint8_t* ev_kind_out, int32_t* ev_t_out) {
   if (n_threads < 1) n_threads = 1;
   if (n_threads > 256) n_threads = 256;
   job_t jobs[256];
@@ -976,6 +987,11 @@ int64_t or_fuzz_label_batch(int64_t seed0, int64_t n, int32_t subtask,
     jobs[i].mode_out = mode_out;
     jobs[i].nev_out = n_events_out;
     jobs[i].nrec_out = n_records_out;
+    jobs[i].flags_out = flags_out;
+    jobs[i].d0_out = d0_out;
+    jobs[i].ev_stride = ev_stride;
+    jobs[i].ev_kind_out = ev_stride > 0 ? ev_kind_out : NULL;
+    jobs[i].ev_t_out = ev_t_out;
     jobs[i].base = seed0;
     jobs[i].records = 0;
   }
@@ -988,4 +1004,12 @@ int64_t or_fuzz_label_batch(int64_t seed0, int64_t n, int32_t subtask,
   int64_t total = 0;
   for (int i = 0; i < n_threads; i++) total += jobs[i].records;
   return total;
+}
+
+int64_t or_fuzz_label_batch(int64_t seed0, int64_t n, int32_t subtask,
+                            const or_fuzz_cfg* cfg, const or_thresholds* th,
+                            int32_t n_threads, uint8_t* mode_out,
+                            int32_t* n_events_out, int64_t* n_records_out) {
+  return or_fuzz_label_batch_ex(seed0, n, subtask, cfg, th, n_threads, mode_out, n_events_out,
+                                n_records_out, NULL, NULL, 0, NULL, NULL);
 }

@@ -164,6 +164,14 @@ def lib():
                                           ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p]
         L.or_fuzz_label_batch.restype = ctypes.c_int64
+        L.or_fuzz_label_batch_ex.argtypes = [ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int32, P(_FuzzCfg),
+                                             P(_Thresholds), ctypes.c_int32,
+                                             ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_int64,
+                                             ctypes.c_void_p, ctypes.c_void_p]
+        L.or_fuzz_label_batch_ex.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -335,3 +343,28 @@ def fuzz_label_batch(seed0, n, subtask, cfg=None, th=None, n_threads=1,
                                       int(n_threads), _ptr(modes), _ptr(nev),
                                       _ptr(nrec))
     return total, modes, nev, nrec
+
+
+def fuzz_label_batch_full(seed0, n, subtask, cfg=None, th=None, n_threads=1):
+    """fuzz -> extract_events -> classify for seeds [seed0, seed0+n): dict of
+    mode, n_events, n_rec, flags (bit 0 success_once, bit 1 success_at_end),
+    d0, and the event lists in CSR form (ev_off, ev_kind, ev_t)."""
+    cfg = cfg or fuzz_cfg()
+    stride = 4 * (1 + (cfg.max_events + 8) * cfg.max_gap + cfg.max_tail + 2)
+    modes = np.zeros(n, np.uint8)
+    nev = np.zeros(n, np.int32)
+    nrec = np.zeros(n, np.int64)
+    flags = np.zeros(n, np.uint8)
+    d0 = np.zeros(n, np.float64)
+    ek = np.zeros(n * stride, np.uint8)
+    et = np.zeros(n * stride, np.int32)
+    lib().or_fuzz_label_batch_ex(int(seed0), int(n), int(subtask), ctypes.byref(cfg),
+                                 ctypes.byref(thresholds(th)), int(n_threads), _ptr(modes),
+                                 _ptr(nev), _ptr(nrec), _ptr(flags), _ptr(d0), stride,
+                                 _ptr(ek), _ptr(et))
+    cnt = np.maximum(nev, 0).astype(np.int64)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(cnt, out=off[1:])
+    take = (np.arange(n * stride) % stride) < np.repeat(cnt, stride)
+    return dict(mode=modes, n_events=nev, n_rec=nrec, flags=flags, d0=d0,
+                ev_off=off, ev_kind=ek[take], ev_t=et[take])

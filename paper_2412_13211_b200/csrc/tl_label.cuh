@@ -426,6 +426,7 @@ __device__ __forceinline__ void stage_cset(tl_cset* dst, const tl_cset* src) {
   static_assert(sizeof(tl_cset) % 4 == 0, "cset size");
   const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
   uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  __syncwarp();  // every lane is done reading the slot's previous cset
   for (int i = lane_id(); i < (int)(sizeof(tl_cset) / 4); i += 32) d[i] = __ldg(s + i);
   __syncwarp();
 }
@@ -933,7 +934,8 @@ __global__ void __launch_bounds__(kLabelWarps * 32, PART == 1 ? TL_LABEL_MINB : 
   const int64_t stride = R.plane_stride;
   const int dof = R.dof;
   const bool vec_ok = (stride & 3) == 0 && (reinterpret_cast<uintptr_t>(R.planes) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(R.grasped) & 3) == 0;
+                      (reinterpret_cast<uintptr_t>(R.grasped) & 3) == 0 &&
+                      (reinterpret_cast<uintptr_t>(step_mask) & 7) == 0;  // word mask stores
   auto fast_ok = [&](int ci, int64_t rs, int n) {
     return sizeof(T) == 4 && DOFMAX == 7 && dof == 7 && !vec_generic && n >= 2 && (rs & 3) == 0 &&
            vec_ok && rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride && csets[ci].rest_zero;

@@ -65,6 +65,11 @@ struct SynthParams {
   uint8_t* ev_kind;
   int32_t* ev_t;
   unsigned long long* ev_state;  // [n_env] look-back status, zeroed per launch
+  // [2] claim counters (episodes, event-list emission), zeroed by the reset
+  // kernel: k_synth_cta takes episodes by ticket, so every cross-CTA wait
+  // targets an episode already claimed by a running CTA (no co-residency
+  // assumption, see ev_emit_all)
+  unsigned int* tickets;
 };
 
 __device__ __forceinline__ bool in_alpha(int k, int ev) {
@@ -383,6 +388,7 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
                          : rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
   const int ms = p.cfg.max_events + 4;
   if (lane == 0) TL_STAMP(0);
+  if (blockIdx.x == 0 && lane == 0 && p.tickets) { p.tickets[0] = 0u; p.tickets[1] = 0u; }
   if (valid) {
     const int64_t seed = p.seeds[e];
     // odd lanes: realize RNG, final state written straight to global memory
@@ -424,6 +430,7 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
 // streamed straight to global memory: no shared memory)
 __global__ void __launch_bounds__(128) k_seed_states(SynthParams p) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e == 0 && p.tickets) { p.tickets[0] = 0u; p.tickets[1] = 0u; }
   if (e < p.n_env) mt_seed_lane_stream(p.scripts[e].seed, p.states + e * kMtN);
 }
 

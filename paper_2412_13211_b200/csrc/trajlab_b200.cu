@@ -11,7 +11,9 @@
 
 #include "tl_common.cuh"
 #include "tl_label.cuh"
-#include "tl_label_tma.cuh"
+#ifdef TL_AB
+#include "tl_label_tma.cuh"  // A/B probe build only (slower TMA-staged labeller)
+#endif
 #include "tl_synth.cuh"
 #include "tl_synth_cta.cuh"
 #include "tl_filter.cuh"
@@ -77,6 +79,14 @@ void set_max_smem(F* k, int bytes) {
   std::lock_guard<std::mutex> g(mu);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
+
+// Launch-shape overrides exist only in the A/B probe build (-DTL_AB,
+// scripts/*_ab.sh); the product library has one code path per config.
+#ifdef TL_AB
+const char* ab_env(const char* name) { return getenv(name); }
+#else
+constexpr const char* ab_env(const char*) { return nullptr; }
+#endif
 
 int blocks_for(int n_items, int per_block, int max_blocks) {
   int b = (n_items + per_block - 1) / per_block;
@@ -203,16 +213,15 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
   // episodes of a 2^20-episode batch, and the episodes in flight stay close
   // in memory (measured: 16/SM 84 %, 128/SM 89 %, one block per 8 episodes 78 %
   // of HBM on the Pick sizing run)
-  const char* gm = getenv("TL_LABEL_GRID_PER_SM");  // A/B measurement only
-  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * (gm ? atoi(gm) : 128));
+  const char* gm = ab_env("TL_LABEL_GRID_PER_SM");
+  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * (gm ? std::max(1, atoi(gm)) : 128));
   const dim3 blk(kLabelWarps * 32);
   const bool small = recs->dof <= 7;
-  // TL_LABEL_TMA=1 selects the shared-memory (TMA bulk copy) staged variant;
-  // it is slower than the register path + L2 bulk prefetch at the occupancy
-  // its buffers allow (profiles/r1_ncu_summary.md), kept for A/B runs.
-  const bool use_tma = getenv("TL_LABEL_TMA") != nullptr;
-  const int vgen = getenv("TL_LABEL_V4GEN") != nullptr;  // A/B: runtime-dof vec4 body
-  if (recs->dtype == 0 && use_tma) {
+  const int vgen = ab_env("TL_LABEL_V4GEN") != nullptr;  // A/B: runtime-dof vec4 body
+#ifdef TL_AB
+  // TL_LABEL_TMA=1: the shared-memory (TMA bulk copy) staged variant, slower
+  // than the register path + L2 bulk prefetch (profiles/r1_ncu_summary.md)
+  if (recs->dtype == 0 && ab_env("TL_LABEL_TMA")) {
     if (small) {
       using SM7 = LabelTmaSmem<7>;
       set_max_smem(k_label_tma<7>, (int)sizeof(SM7));
@@ -226,7 +235,10 @@ int tl_label_records(const tl_records* recs, int32_t n_env, const int32_t* env_c
                         sizeof(SM16), S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask,
                                                    step_success, labels);
     }
-  } else if (recs->dtype == 0) {
+    return check_launch();
+  }
+#endif
+  if (recs->dtype == 0) {
     if (small) {  // vector-body episodes, then everything else (k_label PART 1 / 2)
       k_label<float, 7, 1><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
       k_label<float, 7, 2><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, r, step_mask, step_success, labels, vgen);
@@ -307,11 +319,11 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
 // episodes (measured: scripts/reset_epw_ab.sh, scripts/reset_epw_ab2.sh)
 static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   const int n = sp.n_env, sms = sm_count();
-  const char* force = getenv("TL_RESET_EPW");  // A/B measurement only
+  const char* force = ab_env("TL_RESET_EPW");
   const int epw = force ? atoi(force)
                         : (int64_t)n <= (int64_t)sms * 8 ? 1 : (int64_t)n <= (int64_t)sms * 64 ? 4 : 8;
   // large batches: streamed seeding, one shared-memory row per episode
-  const bool stream_seed = epw >= 2 && getenv("TL_RESET_ROWS2") == nullptr;
+  const bool stream_seed = epw >= 2 && ab_env("TL_RESET_ROWS2") == nullptr;
   const int smem = (stream_seed ? 1 : 2) * epw * kRowWords * 4;
   switch (epw) {
     case 1: k_fuzz_reset<1, false><<<n, 32, smem, S(stream)>>>(sp); break;
@@ -368,7 +380,7 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   // realize + label: one CTA per episode (tl_synth_cta.cuh); 2-warp CTAs
   // (32-record waves) when no episode can exceed 64 records
   const bool small = sp.out.dof <= 7;
-  const char* fw = getenv("TL_SYNTH_WAVE");  // A/B measurement only
+  const char* fw = ab_env("TL_SYNTH_WAVE");
   const int W = fw ? (atoi(fw) == 32 ? 32 : 64)
                    : (sp.cap_per_env > 0 && sp.cap_per_env <= 64 ? 32 : 64);
   const int threads = W + 32;
@@ -385,7 +397,7 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
     k_seed_states<<<(sp.n_env + 127) / 128, 128, 0, S(stream)>>>(sp);
   }
   const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
-  if (getenv("TL_DEBUG"))
+  if (ab_env("TL_DEBUG"))
     fprintf(stderr, "k_synth_cta<W=%d>: %d CTAs/SM (smem %d B, %d threads), grid %d\n", W, per_sm,
             smem, threads, grid);
   k<<<grid, threads, smem, S(stream)>>>(sp);
@@ -398,11 +410,12 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
   const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
   return align256(n * kMtN * 4) + align256(n * sizeof(tl_script)) + align256(n * ms) +
-         align256(n * ms * 4) + align256(n * 8);  // + event look-back states (tl_fuzz_ev)
+         align256(n * ms * 4) + align256(n * 8)  // + event look-back states (tl_fuzz_ev)
+         + 256;                                   // + episode / emission tickets
 }
 
 size_t tl_realize_scratch_bytes(int32_t n_env) {
-  return align256((size_t)(n_env > 0 ? n_env : 1) * kMtN * 4);
+  return align256((size_t)(n_env > 0 ? n_env : 1) * kMtN * 4) + 256;  // states + tickets
 }
 
 static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
@@ -431,6 +444,8 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   sp.step_gap = script_gap ? script_gap : reinterpret_cast<int32_t*>(base);
   base += align256(n * ms * 4);
   sp.ev_state = reinterpret_cast<unsigned long long*>(base);
+  base += align256(n * 8);
+  sp.tickets = reinterpret_cast<unsigned int*>(base);
   sp.seeds = seeds;
   sp.fuzz_subtask = subtask;
   sp.cfg = *cfg;
@@ -489,6 +504,8 @@ int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t
   sp.step_kind = const_cast<uint8_t*>(step_kind);
   sp.step_gap = const_cast<int32_t*>(step_gap);
   sp.states = reinterpret_cast<uint32_t*>(scratch);
+  sp.tickets = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(scratch) +
+                                               align256((size_t)n_env * kMtN * 4));
   sp.n_env = n_env;
   sp.th = *th_realize;
   sp.label_csets = label_csets;
@@ -760,8 +777,8 @@ int tl_eval_predicates(const tl_records* recs, int32_t n_env, const int32_t* env
   // episodes of a 2^20-episode batch, and the episodes in flight stay close
   // in memory (measured: 16/SM 84 %, 128/SM 89 %, one block per 8 episodes 78 %
   // of HBM on the Pick sizing run)
-  const char* gm = getenv("TL_LABEL_GRID_PER_SM");  // A/B measurement only
-  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * (gm ? atoi(gm) : 128));
+  const char* gm = ab_env("TL_LABEL_GRID_PER_SM");
+  const int grid = blocks_for(n_env, kLabelWarps, sm_count() * (gm ? std::max(1, atoi(gm)) : 128));
   const dim3 blk(kLabelWarps * 32);
   if (recs->dtype == 0) {
     if (recs->dof <= 7) k_predicates<float, 7><<<grid, blk, 0, S(stream)>>>(*recs, n_env, env_cset, csets, a0, bits, errs, jmax);
