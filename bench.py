@@ -1,21 +1,28 @@
 """Benchmark of the B200 hot path: batched env reset/step (random_script +
-realize) fused with event labelling and mode classification, plus event
-list emission (and, for N>1, the NCCL label all-gather + mode-histogram
-all-reduce).
+realize) fused with event labelling, mode classification and ordered event
+list emission (and, for N>1, the NCCL label all-gather + global mode
+histogram).
 
-Workload (BASELINE.json configs[1], "C2"): Place skill, 1024 parallel envs
-per GPU; each env runs one random-action rollout = fuzz(seed, Place,
-FuzzConfig(max_gap=64, max_tail=64)) (~200 env steps); every bench step
-uses fresh seeds.  Metric: env samples/sec (records generated + labelled
-per second, whole job), with labelled trajectories/sec alongside.
+Headline workload (BASELINE.json configs[1] "C2" rollouts at the north-star
+size): Place skill, 4096 parallel envs PER GPU; each env runs one
+random-action rollout = fuzz(seed, Place, FuzzConfig(max_gap=64,
+max_tail=64)) (~175 env steps); every bench step uses fresh, rank-disjoint
+seeds.  Metric: env samples/sec (records generated + labelled per second,
+whole job), with labelled trajectories/sec alongside.  C2 at 1024 envs, C3
+(Open/Close, 4096 envs/GPU), C4, C5, the env API and the label sizing run are
+extra keys.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run (one process per GPU, NCCL, 127.0.0.1).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -26,25 +33,102 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_ENV = 1024
-KIND = 1  # Place
+N_ENV = 4096                 # envs per GPU (north star: >= 4096 per GPU)
+KIND = 1                     # Place
 CFG = dict(max_events=8, max_gap=64, max_tail=64, edge_density=1.0, success_prob=0.5)
-RECORD_BYTES = 93  # 23 f32 planes + 1 u8 grasped (dof 7), SURVEY 8(d)
+RECORD_BYTES = 93            # 23 f32 planes + 1 u8 grasped (dof 7), SURVEY 8(d)
 LABEL_BYTES = 24
-WORKLOAD = ("C2: Place, 1024 envs/GPU, random-action rollout per env = "
-            "fuzz(seed, Place, FuzzConfig(max_gap=64, max_tail=64)) (~200 steps), "
-            "fresh seeds every step; generation + events + modes (+ event lists)")
 METRIC = "env samples/sec (SPS)"
+WORKLOAD = ("Place random-action rollouts, 4096 envs per GPU: every env runs "
+            "fuzz(seed, Place, FuzzConfig(max_gap=64, max_tail=64)) (~175 env steps; the "
+            "BASELINE C2 rollout at the north-star per-GPU size), fresh rank-disjoint seeds "
+            "every step; generation + events + modes + ordered event lists")
 
 
-def parse():
+def bench_config(world):
+    """The config dict BOTH arms print (the driver compares them)."""
+    return {"workload": WORKLOAD, "envs_per_gpu": N_ENV, "subtask": "Place",
+            "fuzz_config": dict(CFG),
+            "seeds": "step k, rank r: [(k*N + r)*4096, (k*N + r + 1)*4096)",
+            "parallelism": f"episodes (seeds) sharded over {world} GPU(s); labels all-gathered "
+                           "over NCCL when N > 1",
+            "l2": "flushed between timed steps (256 MiB write, excluded from timing)"}
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
+    ap.add_argument("--no-extras", action="store_true",
+                    help="headline only (skip C2/C3/C4/C5/env/sizing side runs)")
+    return ap.parse_args(argv)
+
+
+# ---- multi-GPU plumbing (covered on CPU by tests/test_bench_dist.py) ----------
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_argv(n, argv, port):
+    """torchrun command that re-runs this script with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__), *argv]
+
+
+def maybe_self_launch(args, argv):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run.
+    NCCL's init log (nranks) goes to stderr."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return subprocess.call(launch_argv(args.gpus, argv, free_port()), env=env)
+
+
+def rank_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def step_seeds(k, rank, world, n_env=N_ENV):
+    """seeds of bench step k on rank r: contiguous, rank-disjoint, fresh per step"""
+    return (k * world + rank) * n_env + np.arange(n_env, dtype=np.int64)
+
+
+def max_over_ranks(values, world, device=None):
+    """element-wise max over ranks (the timing rule: the slowest rank)"""
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t.tolist()
+
+
+def sum_over_ranks(values, world, device=None):
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t)
+    return t.tolist()
+
+
+def gather_labels(local, out, world):
+    """the one exchange step: rank-ordered all-gather of the
+    24-byte labels (rank order = episode_id order)"""
+    import torch
+    if world == 1:
+        out.copy_(local.view(out.shape))
+        return out
+    torch.distributed.all_gather_into_tensor(out.view(-1), local.reshape(-1))
+    return out
 
 
 class ClockSampler:
@@ -107,18 +191,26 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def profile_traffic():
-    """dram bytes/launch of k_synth from the committed ncu capture, if any."""
+def profile_json(name):
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            d = json.load(f)
-        return d.get("k_synth_dram_bytes_per_launch"), d.get("k_synth_records_per_launch")
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
     except Exception:
-        return None, None
+        return None
+
+
+def latency_constants():
+    """critical-path cycle costs measured by scripts/floor_probe.cu on a B200
+    (profiles/r2_floor_probe.json)"""
+    d = profile_json("r2_floor_probe.json")
+    if d:
+        return float(d["cycles_per_seed_step"]), float(d["cum_cycles_per_record"]), \
+            "profiles/r2_floor_probe.json (scripts/floor_probe.cu)"
+    return 20.0, 72.0, "round-1 estimates (DESIGN.md section 9)"
 
 
 def host_info():
-    """The host the CPU baseline ran on (core count, CPU model, Python)."""
+    """The host the CPU baselines ran on (core count, CPU model, Python)."""
     import platform
     model = platform.processor() or ""
     try:
@@ -132,11 +224,16 @@ def host_info():
     return {"cpu_count": os.cpu_count(), "cpu_model": model, "python": platform.python_version()}
 
 
+def oracle_cfg():
+    from oracle import oracle as O
+    return O.fuzz_cfg(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail", "edge_density",
+                                             "success_prob")})
+
+
 def cpu_baseline(seconds, n_threads=1):
     """CPU oracle (C restatement of the reference path) on a bounded sample."""
     from oracle import oracle as O
-    cfg = O.fuzz_cfg(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail", "edge_density",
-                                            "success_prob")})
+    cfg = oracle_cfg()
     n, recs, t = 64, 0, 0.0
     seed = 10 ** 9
     while t < seconds:
@@ -150,16 +247,113 @@ def cpu_baseline(seconds, n_threads=1):
     return recs / t, eps / t, f"{eps} episodes ({recs} env steps) of the bench workload, {t:.1f} s"
 
 
+# ---- the reference's own Python implementation (baseline/_ref) ----------------
+def reference_path():
+    """where the unmodified reference package is importable from: the offline
+    install baseline/_ref (travels to the GPU box), else the source tree"""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isfile(os.path.join(p, "trajlab", "__init__.py")):
+            return p
+    return None
+
+
+def _pyref_chunk(job):
+    """Pool worker: the reference's fuzz -> extract_events -> classify over a
+    seed chunk (what label_batch's workers do per trajectory,
+    pipeline.py:75-94, 134-138)."""
+    path, s0, s1 = job
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import trajlab as T
+    cfg = T.FuzzConfig(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail")})
+    th = T.Thresholds()
+    recs = 0
+    for s in range(s0, s1):
+        tr = T.fuzz(s, T.SubtaskKind.Place, cfg)
+        T.classify(T.extract_events(tr, th))
+        recs += len(tr.records)
+    return recs
+
+
+def python_reference_baseline(seconds=4.0):
+    """SURVEY 8(d) CPU reference timing with the REAL reference (pure Python,
+    baseline/_ref): (i) one core, generation (fuzz) and labelling
+    (classify(extract_events(.))) timed separately; (ii) all cores,
+    multiprocessing.Pool over contiguous seed chunks; (iii) the file path
+    label_batch(paths, workers=os.cpu_count()) over TRJL1 files."""
+    import multiprocessing
+    import tempfile
+    path = reference_path()
+    if path is None:
+        return {"unavailable": "reference package not installed in baseline/_ref"}
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import trajlab as T
+    cores = os.cpu_count() or 1
+    cfg = T.FuzzConfig(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail")})
+    th = T.Thresholds()
+    # (i) single core, generation and labelling separately
+    seed, recs, t_gen, t_lab, trajs = 2 * 10 ** 9, 0, 0.0, 0.0, []
+    while t_gen + t_lab < seconds:
+        t0 = time.perf_counter()
+        tr = T.fuzz(seed, T.SubtaskKind.Place, cfg)
+        t1 = time.perf_counter()
+        T.classify(T.extract_events(tr, th))
+        t2 = time.perf_counter()
+        t_gen += t1 - t0
+        t_lab += t2 - t1
+        recs += len(tr.records)
+        if len(trajs) < 1000:
+            trajs.append(tr)
+        seed += 1
+    n1 = seed - 2 * 10 ** 9
+    one = {"generate_sps": recs / t_gen, "label_sps": recs / t_lab,
+           "fuzz_and_label_sps": recs / (t_gen + t_lab),
+           "sample": f"{n1} episodes ({recs} env steps), one core, {t_gen + t_lab:.1f} s"}
+    # (ii) all cores: Pool over contiguous seed chunks (label_batch's pattern)
+    per_ep = (t_gen + t_lab) / n1
+    chunk = max(1, int(seconds / per_ep / 4))
+    jobs = [(path, 3 * 10 ** 9 + i * chunk, 3 * 10 ** 9 + (i + 1) * chunk) for i in range(4 * cores)]
+    ctx = multiprocessing.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_pyref_chunk, [(path, 0, 1)] * cores)       # workers imported
+        t0 = time.perf_counter()
+        r = sum(pool.map(_pyref_chunk, jobs, chunksize=1))
+        t_pool = time.perf_counter() - t0
+    pool_d = {"fuzz_and_label_sps": r / t_pool, "workers": cores,
+              "sample": f"{len(jobs) * chunk} episodes ({r} env steps), Pool({cores}), {t_pool:.1f} s"}
+    # (iii) label_batch over TRJL1 files, all cores
+    with tempfile.TemporaryDirectory() as d:
+        paths = []
+        frecs = 0
+        for i, tr in enumerate(trajs):
+            p = os.path.join(d, f"{i:06d}.trjl")
+            T.write_binary_file(tr, p)
+            paths.append(p)
+            frecs += len(tr.records)
+        t0 = time.perf_counter()
+        res = T.label_batch(paths, workers=cores)
+        t_lb = time.perf_counter() - t0
+    lb = {"label_sps": frecs / t_lb, "workers": cores, "ok": res.ok,
+          "sample": f"label_batch over {len(paths)} TRJL1 files ({frecs} env steps), {t_lb:.2f} s"}
+    import platform
+    return {"kind": "reference-python", "package": os.path.relpath(path, ROOT) if path.startswith(ROOT) else path,
+            "single_core": one, "pool": pool_d, "label_batch": lb, "cores": cores,
+            "python": platform.python_version(), "workload": "fuzz(seed, Place, FuzzConfig(max_gap=64, "
+            "max_tail=64)) -> extract_events -> classify, seeds from 2e9 / 3e9"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference path's CPU implementation (the C
-    oracle port, all host threads) on the same workload."""
+    restatement oracle/oracle.c, all host threads) on the same workload, the
+    same config and seeds as the GPU arm; plus the real Python reference timed
+    beside it (python_reference)."""
     if rank != 0:
         return
     from oracle import oracle as O
     cores = os.cpu_count() or 1
-    cfg = O.fuzz_cfg(**{k: CFG[k] for k in ("max_events", "max_gap", "max_tail", "edge_density",
-                                            "success_prob")})
-    n_env = N_ENV * world
+    cfg = oracle_cfg()
+    n_env = N_ENV * world   # the whole job's episodes per step (weak scaling)
     for k in range(args.warmup):
         O.fuzz_label_batch(-(k + 1) * n_env - 10 ** 8, n_env, KIND, cfg, n_threads=cores, want_outputs=False)
     recs, t0 = 0, time.perf_counter()
@@ -168,19 +362,21 @@ def run_reference(args, rank, world):
         recs += r
     dt = time.perf_counter() - t0
     sps = recs / dt
+    pyref = python_reference_baseline()
     out = {"impl": "reference", "metric": METRIC, "value": sps, "unit": "env-steps/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "trajectories_per_sec": n_env * args.steps / dt,
-           "config": {"workload": WORKLOAD, "envs_per_step": n_env},
+           "config": bench_config(world),
            "cpu_baseline": {"value": sps, "unit": "env-steps/s", "cores": cores, "kind": "port",
                             "sample": f"{args.steps} steps x {n_env} episodes, oracle/oracle.c "
                                       "(C restatement of trajlab fuzz+extract_events+classify), "
                                       f"{cores} threads", "host": host_info()},
+           "python_reference": pyref,
            "e2e": {"value": sps, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
 LABEL_READ_BYTES = {"pick": 81.0, "place": 85.0, "open": 88.0, "close": 88.0}
@@ -350,23 +546,23 @@ def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
         torch.cuda.synchronize()
         if k:
             ms.append(a.elapsed_time(b))
-    t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    t = float(t.item()) / 1e3
+    t = max_over_ranks([sum(ms) / len(ms)], world, dev)[0] / 1e3
     n_total = 4 * n_per_subtask
     return {"workload": "C5: fuzz 4 x 250k episodes (default FuzzConfig) -> label -> "
                         "all-gather -> filter_labels (A.6.1 recipe, quota 1000/target)",
             "episodes": n_total, "n_gpus": world, "ms": 1e3 * t,
             "labelled_trajectories_per_s": n_total / t,
             "selected": int(sum(man.pool_selected)), "pools": len(man.pools),
-            "timing": "CUDA events around the whole pipeline (incl. host glue), max over ranks"}
+            "timing": "CUDA events around the whole pipeline (incl. host glue), max over ranks",
+            "parity": "tests/test_gpu_shipped.py::test_c5_bench_scale_filter_vs_oracle"}
 
 
-def fuzz_step_graph(dev, stream, n_env, kind, cfg):
+def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None):
     """One fused fuzz step (tl_fuzz_ev: reset + realize + labels + ordered
-    event lists) on preallocated buffers, captured as a CUDA graph.  Returns
-    (graph, seeds_buf, workspace)."""
+    event lists) on preallocated buffers, captured as a CUDA graph.  host_out
+    (pinned host tensors ev_off / ev_kind / ev_t, optionally labels): the
+    kernel writes those outputs straight into host memory (zero-copy).
+    Returns (graph, seeds_buf, workspace, device event buffers)."""
     import ctypes
     import torch
     from paper_2412_13211_b200 import _lib as L
@@ -384,13 +580,17 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg):
     bufs = dict(ev_off=torch.empty(n_env + 1, dtype=torch.int64, device=dev),
                 ev_kind=torch.empty(ev_cap, dtype=torch.uint8, device=dev),
                 ev_t=torch.empty(ev_cap, dtype=torch.int32, device=dev))
+    out = dict(bufs)
+    out["labels"] = ws.labels
+    if host_out:
+        out.update(host_out)
     rb_c = ws.records().c()
 
     def body(s):
         L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), n_env, kind, ctypes.byref(cfg_c),
                                ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
-                               None, None, None, L.ptr(ws.step_mask), L.ptr(ws.labels),
-                               L.ptr(bufs["ev_off"]), L.ptr(bufs["ev_kind"]), L.ptr(bufs["ev_t"]),
+                               None, None, None, L.ptr(ws.step_mask), L.ptr(out["labels"]),
+                               L.ptr(out["ev_off"]), L.ptr(out["ev_kind"]), L.ptr(out["ev_t"]),
                                ev_cap, L.ptr(ws.scratch), ctypes.c_void_p(s.cuda_stream)),
                 "tl_fuzz_ev")
     body(stream)
@@ -398,8 +598,33 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         body(torch.cuda.current_stream())
-    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf)  # the graph reads these
-    return g, seeds_buf, ws
+    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf, out)  # the graph reads these
+    return g, seeds_buf, ws, bufs
+
+
+def fuzz_batch_timed(dev, stream, world, flush, n_env, kind, cfg, reps):
+    """device time per fuzz batch (graph replay, L2 flushed), max over ranks"""
+    import torch
+    rank = torch.distributed.get_rank() if world > 1 else 0
+    g, seeds_buf, ws, _ = fuzz_step_graph(dev, stream, n_env, kind, cfg)
+    ms, recs = [], 0
+    for k in range(reps + 2):
+        seeds_buf.copy_(torch.from_numpy(step_seeds(k + 7919, rank, world, n_env)).to(dev))
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k >= 2:
+            ms.append(a.elapsed_time(b))
+            recs += int(ws.n_rec.sum())
+    t = max_over_ranks([sum(ms) / len(ms)], world, dev)[0] / 1e3
+    recs = sum_over_ranks([recs / reps], world, dev)[0]
+    lab = ws.labels.cpu().numpy().reshape(-1).view(L_LABEL_DTYPE())
+    return {"ms": 1e3 * t, "env_steps_per_s": recs / t,
+            "labelled_trajectories_per_s": n_env * world / t,
+            "mean_steps": recs / (n_env * world), "failed": int((lab["status"] != 0).sum())}
 
 
 def c3_run(dev, stream, world, flush, n_env=4096, reps=20):
@@ -408,40 +633,22 @@ def c3_run(dev, stream, world, flush, n_env=4096, reps=20):
     rank-disjoint seeds every batch, default FuzzConfig; generation + labels +
     ordered event lists (tl_fuzz_ev, one CUDA graph per batch), device-timed
     per batch with L2 flushed between batches, max over ranks."""
-    import torch
     import paper_2412_13211_b200 as P
-    rank = torch.distributed.get_rank() if world > 1 else 0
-    cfg = P.FuzzConfig()
-    out = {}
-    for name, kind in (("open", 2), ("close", 3)):
-        g, seeds_buf, ws = fuzz_step_graph(dev, stream, n_env, kind, cfg)
-        ms, recs = [], 0
-        for k in range(reps + 2):
-            seeds_buf.copy_(torch.arange(n_env, dtype=torch.int64, device=dev)
-                            + (k * world + rank) * n_env)
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            g.replay()
-            b.record(stream)
-            torch.cuda.synchronize()
-            if k >= 2:
-                ms.append(a.elapsed_time(b))
-                recs += int(ws.n_rec.sum())
-        t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t = float(t.item()) / 1e3
-        recs /= reps
-        lab = ws.labels.cpu().numpy().reshape(-1).view(L_LABEL_DTYPE())
-        out[name] = {"ms": 1e3 * t, "env_steps_per_s": recs * world / t,
-                     "labelled_trajectories_per_s": n_env * world / t,
-                     "mean_steps": recs / n_env, "failed": int((lab["status"] != 0).sum())}
-        del g, ws
+    out = {name: fuzz_batch_timed(dev, stream, world, flush, n_env, kind, P.FuzzConfig(), reps)
+           for name, kind in (("open", 2), ("close", 3))}
     out["workload"] = ("C3: fuzz(seed, Open|Close), 4096 envs/GPU each, default FuzzConfig, "
                        "fresh seeds per batch, generation + labels + ordered event lists "
                        "(tl_fuzz_ev, CUDA graph), L2 flushed between batches")
     return out
+
+
+def c2_run(dev, stream, world, flush, reps=20):
+    """BASELINE C2 exactly: Place, 1024 envs per GPU, max_gap = max_tail = 64"""
+    import paper_2412_13211_b200 as P
+    r = fuzz_batch_timed(dev, stream, world, flush, 1024, KIND, P.FuzzConfig(**CFG), reps)
+    r["workload"] = ("C2: Place, 1024 envs/GPU, fuzz(seed, Place, FuzzConfig(max_gap=64, "
+                     "max_tail=64)), tl_fuzz_ev CUDA graph, L2 flushed between batches")
+    return r
 
 
 def L_LABEL_DTYPE():
@@ -501,7 +708,7 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
     subs = ["Open", "Pick", "Place", "Close"]
     graphs = []
     for si, sub in enumerate(subs):   # label rows [2n*si, 2n*(si+1)): rep 0 then rep 1
-        g, seeds_buf, ws = fuzz_step_graph(dev, stream, 2 * n_chain, sub_idx[sub], cfg)
+        g, seeds_buf, ws, _ = fuzz_step_graph(dev, stream, 2 * n_chain, sub_idx[sub], cfg)
         seeds_buf.copy_(torch.cat([8 * chains + 4 * rep + order[sub] for rep in (0, 1)]))
         graphs.append((g, ws))
     slot_label = torch.full((n_chain, len(plan)), -1, dtype=torch.int64, device=dev)
@@ -531,7 +738,7 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
         torch.cuda.synchronize()
         if k:
             ms.append(a.elapsed_time(b))
-    t = sum(ms) / len(ms) / 1e3
+    t = max_over_ranks([sum(ms) / len(ms)], world, dev)[0] / 1e3
     curve = [100.0 * int(x) / (n_chain * world) for x in alive.cpu().tolist()]
     return {"workload": "C4: SetTable chains (settable plan, 16 slots), 4096 chains/GPU, "
                         "8 fuzz episodes per chain (seeds 8c+k), one fused fuzz graph per "
@@ -542,11 +749,38 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
             "progressive_completion": curve}
 
 
-def main():
-    args = parse()
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
+def self_check(ws, ev_host, seeds):
+    """the timed kernels' last outputs against the CPU oracle (oracle/, test
+    infrastructure): every label field and the ordered event lists"""
+    from oracle import oracle as O
+    from paper_2412_13211_b200 import _lib as L
+    lab = ws.labels.cpu().numpy().reshape(-1).view(L.LABEL_DTYPE)
+    nrec = ws.n_rec.cpu().numpy()
+    want = O.fuzz_label_batch_full(int(seeds[0]), len(seeds), KIND, oracle_cfg(),
+                                   n_threads=os.cpu_count() or 1)
+    off = ev_host["ev_off"].numpy()
+    tot = int(off[-1])
+    ok = (bool(np.all(lab["status"] == 0)) and np.array_equal(lab["mode"], want["mode"])
+          and np.array_equal(lab["flags"] & 3, want["flags"])
+          and np.array_equal(lab["n_events"], want["n_events"])
+          and np.array_equal(nrec.astype(np.int64), want["n_rec"])
+          and np.array_equal(off, want["ev_off"])
+          and np.array_equal(ev_host["ev_kind"].numpy()[:tot], want["ev_kind"])
+          and np.array_equal(ev_host["ev_t"].numpy()[:tot], want["ev_t"]))
+    if not ok:
+        raise RuntimeError("bench self-check: GPU labels / event lists differ from the oracle")
+    return {"episodes": len(seeds), "events": tot, "vs": "oracle/oracle.c fuzz -> extract_events "
+            "-> classify on the same seeds", "fields": "status, mode, flags, n_events, n_rec, "
+            "ev_off, ev_kind, ev_t", "ok": True}
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    rc = maybe_self_launch(args, argv)
+    if rc is not None:
+        sys.exit(rc)
+    rank, world, local = rank_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -555,7 +789,6 @@ def main():
     from paper_2412_13211_b200 import _lib as L
     from paper_2412_13211_b200 import core
     from paper_2412_13211_b200.synth import FuzzConfig
-    from paper_2412_13211_b200.thresholds import Thresholds
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -566,75 +799,44 @@ def main():
     lib = L.lib()
     cfg = FuzzConfig(**CFG)
     cap = core.fuzz_capacity(cfg)
-    ws = core.SynthWorkspace(N_ENV, cap)
-    cs = core.synth_csets(Thresholds()).to_device(dev)
-    th_c = core.thresholds_c(Thresholds())
-    cfg_c = L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0, cfg.edge_density,
-                        cfg.success_prob)
     K, W = args.steps, args.warmup
-    # inputs resident in HBM: seeds of every step, rank-disjoint ranges
-    all_seeds = (torch.arange(K + W, device=dev, dtype=torch.int64)[:, None] * world + rank) * N_ENV \
-        + torch.arange(N_ENV, device=dev, dtype=torch.int64)[None, :]
-    seeds_buf = torch.empty(N_ENV, dtype=torch.int64, device=dev)
-    ev_cap = 4 * N_ENV * cap   # tl_fuzz_ev bound: <= 4 events per record
-    ev_off = torch.empty(N_ENV + 1, dtype=torch.int64, device=dev)
-    ev_kind = torch.empty(ev_cap, dtype=torch.uint8, device=dev)
-    ev_t = torch.empty(ev_cap, dtype=torch.int32, device=dev)
-    scan_scratch = torch.empty(max(16, lib.tl_scan_scratch_bytes(N_ENV)), dtype=torch.uint8, device=dev)
-    hist = torch.zeros(L.N_MODES, dtype=torch.int64, device=dev)
-    gathered = torch.empty((world, N_ENV, 24), dtype=torch.uint8, device=dev) if world > 1 else None
-    rb = ws.records()
-    rb_c = rb.c()
     stream = torch.cuda.Stream(device=dev)  # graphs need a non-default stream
     torch.cuda.set_stream(stream)
-
-    def synth_only(s):
-        # reset kernel + realize kernel; the realize kernel also builds the
-        # ordered event lists (decoupled look-back over episodes)
-        sp = ctypes.c_void_p(s.cuda_stream)
-        L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), N_ENV, KIND, ctypes.byref(cfg_c),
-                               ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
-                               None, None, None, L.ptr(ws.step_mask), L.ptr(ws.labels),
-                               L.ptr(ev_off), L.ptr(ev_kind), L.ptr(ev_t), ev_cap,
-                               L.ptr(ws.scratch), sp), "tl_fuzz_ev")
-
-    def step_body(s):
-        synth_only(s)
-
-    launches_per_step = 2 + (1 if world > 1 else 0)  # reset, realize(+events) [, histogram]
-
-    # warm-up (also sets kernel attributes before graph capture)
-    seeds_buf.copy_(all_seeds[0])
-    step_body(stream)
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        step_body(torch.cuda.current_stream())
-
+    ev_cap = 4 * N_ENV * cap   # tl_fuzz_ev bound: <= 4 events per record
+    # pinned host outputs the e2e path writes into (zero-copy event lists)
+    ev_host = dict(ev_off=torch.empty(N_ENV + 1, dtype=torch.int64).pin_memory(),
+                   ev_kind=torch.empty(ev_cap, dtype=torch.uint8).pin_memory(),
+                   ev_t=torch.empty(ev_cap, dtype=torch.int32).pin_memory())
+    graph, seeds_buf, ws, ev_dev = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg)
+    graph_h, seeds_h, ws_h, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg, host_out=ev_host)
+    hist = torch.zeros(L.N_MODES, dtype=torch.int64, device=dev)
+    gathered = torch.empty((world * N_ENV, 24), dtype=torch.uint8, device=dev)
+    # inputs resident in HBM: seeds of every step, rank-disjoint ranges
+    all_seeds = torch.from_numpy(np.stack([step_seeds(k, rank, world) for k in range(K + W)])).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def collectives():
+    def exchange(labels):
         # the one exchange step: all-gather the 24-byte labels
-        # over NCCL; every rank then builds the global mode histogram from the
-        # gathered labels itself (no second collective)
+        # over NCCL; every rank builds the global mode histogram itself
         if world > 1:
-            dist.all_gather_into_tensor(gathered.view(-1), ws.labels.view(-1))
+            gather_labels(labels, gathered, world)
             L.check(lib.tl_mode_histogram(L.ptr(gathered), world * N_ENV, L.ptr(hist),
                                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
                     "hist")
 
+    launches_per_step = 2 + (1 if world > 1 else 0)  # reset, realize(+events) [, histogram]
     for k in range(W):
         seeds_buf.copy_(all_seeds[K + k])
         graph.replay()
-        collectives()
+        exchange(ws.labels)
     torch.cuda.synchronize()
 
-    # ---- device-timed steps: inputs in HBM, L2 flushed between steps -------
-    nrec_log = torch.empty((K, N_ENV), dtype=torch.int32, device=dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     gpu_id = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) if \
         os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    nrec_log = torch.empty((K, N_ENV), dtype=torch.int32, device=dev)
     with ClockSampler(gpu_id) as clocks:
+        # ---- device-timed steps: inputs in HBM, L2 flushed between steps -------
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -642,7 +844,7 @@ def main():
             ev[k][0].record(stream)
             seeds_buf.copy_(all_seeds[k])
             graph.replay()
-            collectives()
+            exchange(ws.labels)
             ev[k][1].record(stream)
             nrec_log[k].copy_(ws.n_rec)
             flush.zero_()
@@ -651,183 +853,173 @@ def main():
             dist.barrier()
         step_ms = [a.elapsed_time(b) for a, b in ev]
 
-        # ---- k_synth alone (roofline of the dominant kernel) ---------------
+        # ---- the two generator kernels alone (roofline of the dominant work)
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         for k in range(K):
             seeds_buf.copy_(all_seeds[k])
             kev[k][0].record(stream)
-            synth_only(stream)
+            graph.replay()
             kev[k][1].record(stream)
             flush.zero_()
         torch.cuda.synchronize()
         synth_ms = [a.elapsed_time(b) for a, b in kev]
 
-        # ---- end to end through the C ABI with host buffers ---------------
-        # E (headline): pinned host seeds -> GPU -> labels + event lists back
-        # to pinned host memory; records stay in HBM (the rollout buffer).
-        # E_records: additionally compacts the records and copies them back.
+        # ---- end to end through the C ABI with host buffers (wall clock) ---
+        # E: pinned host seeds -> GPU (H2D), the fused kernels write the event
+        # lists into pinned host memory (zero-copy), labels come back by a D2H
+        # copy (N>1: after the NCCL all-gather + histogram, which also comes
+        # back); perf_counter around call + synchronize, per step.
+        # E_records: additionally tl_scan_counts + tl_compact_records into one
+        # contiguous staging buffer [23 planes x R f32 | R grasped u8] and ONE
+        # D2H copy of it (+ the record offsets).
         host_seeds = all_seeds.cpu().pin_memory()
-        comp_planes = torch.empty((23, N_ENV * cap), dtype=torch.float32, device=dev)
-        comp_g = torch.empty(N_ENV * cap, dtype=torch.uint8, device=dev)
+        h_labels = torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory()
+        h_hist = torch.empty(L.N_MODES, dtype=torch.int64).pin_memory()
+        h_tot = torch.empty(1, dtype=torch.int64).pin_memory()
+        staging = torch.empty(N_ENV * cap * RECORD_BYTES + 64, dtype=torch.uint8, device=dev)
+        h_staging = torch.empty(staging.numel(), dtype=torch.uint8).pin_memory()
         comp_start = torch.empty(N_ENV + 1, dtype=torch.int64, device=dev)
         comp_nrec = torch.empty(N_ENV, dtype=torch.int32, device=dev)
-        comp_c = L.Records_c(comp_planes.data_ptr(), comp_g.data_ptr(), comp_start.data_ptr(),
-                             comp_nrec.data_ptr(), N_ENV * cap, 0, 7)
-        h_planes = torch.empty((23, N_ENV * cap), dtype=torch.float32).pin_memory()
-        h_g = torch.empty(N_ENV * cap, dtype=torch.uint8).pin_memory()
-        h_labels = torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory()
-        h_evoff = torch.empty(N_ENV + 1, dtype=torch.int64).pin_memory()
-        h_evk = torch.empty(ev_cap, dtype=torch.uint8).pin_memory()
-        h_evt = torch.empty(ev_cap, dtype=torch.int32).pin_memory()
-        h_tot = torch.empty(2, dtype=torch.int64).pin_memory()
+        h_start = torch.empty(N_ENV + 1, dtype=torch.int64).pin_memory()
+        scan_scratch = torch.empty(max(16, lib.tl_scan_scratch_bytes(N_ENV)), dtype=torch.uint8, device=dev)
+        rb_c = ws_h.records().c()
         K2 = max(1, min(K, 50))
-        # single GPU: the realize kernel writes labels and ordered event lists
-        # straight into pinned host memory (zero-copy over PCIe; UVA makes the
-        # pinned buffers device-addressable), so a step needs one sync, not a
-        # sync + sized copies.  N > 1 keeps device labels for the NCCL gather.
-        graph_zc = None
-        if world == 1:
-            def synth_zc(s):
-                sp = ctypes.c_void_p(s.cuda_stream)
-                L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), N_ENV, KIND, ctypes.byref(cfg_c),
-                                       ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c),
-                                       cap, None, None, None, L.ptr(ws.step_mask),
-                                       L.ptr(h_labels), L.ptr(h_evoff), L.ptr(h_evk),
-                                       L.ptr(h_evt), ev_cap, L.ptr(ws.scratch), sp), "tl_fuzz_ev")
-            synth_zc(stream)
-            torch.cuda.synchronize()
-            graph_zc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph_zc, stream=stream):
-                synth_zc(torch.cuda.current_stream())
 
         def e2e_loop(with_records):
-            ms, recs, h2d, d2h = [], 0, 0, 0
+            wall, recs, h2d, d2h = 0.0, 0, 0, 0
             for k in range(K2):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                seeds_buf.copy_(host_seeds[k], non_blocking=True)
-                if graph_zc is not None and not with_records:
-                    graph_zc.replay()   # labels + event lists land in pinned host memory
-                    b.record(stream)
-                    stream.synchronize()
-                    ms.append(a.elapsed_time(b))
-                    recs += int(nrec_log[k].sum())
-                    NE = int(h_evoff[N_ENV])
-                    h2d = N_ENV * 8
-                    d2h = N_ENV * 24 + (N_ENV + 1) * 8 + NE * 5
-                    flush.zero_()
-                    continue
-                graph.replay()
-                collectives()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                seeds_h.copy_(host_seeds[k], non_blocking=True)
+                graph_h.replay()                          # event lists -> pinned host
+                exchange(ws_h.labels)
+                h_labels.copy_(ws_h.labels, non_blocking=True)
+                d2h_k = N_ENV * 24
+                if world > 1:
+                    h_hist.copy_(hist, non_blocking=True)
+                    d2h_k += L.N_MODES * 8
                 sp = ctypes.c_void_p(stream.cuda_stream)
-                h_labels.copy_(ws.labels, non_blocking=True)
-                h_evoff.copy_(ev_off, non_blocking=True)
+                R = 0
                 if with_records:
-                    L.check(lib.tl_scan_counts(L.ptr(ws.n_rec), N_ENV, L.ptr(comp_start),
+                    L.check(lib.tl_scan_counts(L.ptr(ws_h.n_rec), N_ENV, L.ptr(comp_start),
                                                L.ptr(scan_scratch), sp), "scan")
-                    L.check(lib.tl_compact_records(ctypes.byref(rb_c), N_ENV, L.ptr(comp_start),
-                                                   ctypes.byref(comp_c), sp), "compact")
-                    h_tot[0:1].copy_(comp_start[N_ENV:N_ENV + 1], non_blocking=True)
-                stream.synchronize()  # sizes of the variable-length outputs
-                NE = int(h_evoff[N_ENV])
-                R = int(h_tot[0]) if with_records else 0
-                h_evk[:NE].copy_(ev_kind[:NE], non_blocking=True)
-                h_evt[:NE].copy_(ev_t[:NE], non_blocking=True)
-                if with_records:
-                    for p_ in range(23):
-                        h_planes[p_, :R].copy_(comp_planes[p_, :R], non_blocking=True)
-                    h_g[:R].copy_(comp_g[:R], non_blocking=True)
-                b.record(stream)
+                    h_tot.copy_(comp_start[N_ENV:N_ENV + 1], non_blocking=True)
                 stream.synchronize()
-                ms.append(a.elapsed_time(b))
+                if with_records:
+                    R = int(h_tot[0])
+                    base = staging.data_ptr()
+                    dst = L.Records_c(base, base + 23 * 4 * R, comp_start.data_ptr(),
+                                      comp_nrec.data_ptr(), R, 0, 7)
+                    L.check(lib.tl_compact_records(ctypes.byref(rb_c), N_ENV, L.ptr(comp_start),
+                                                   ctypes.byref(dst), sp), "compact")
+                    h_staging[:RECORD_BYTES * R].copy_(staging[:RECORD_BYTES * R], non_blocking=True)
+                    h_start.copy_(comp_start, non_blocking=True)
+                    stream.synchronize()
+                    d2h_k += RECORD_BYTES * R + (N_ENV + 1) * 8 + 8
+                wall += time.perf_counter() - t0
+                NE = int(ev_host["ev_off"][N_ENV])
                 recs += int(nrec_log[k].sum())
                 h2d = N_ENV * 8
-                d2h = N_ENV * 24 + (N_ENV + 1) * 8 + NE * 5 + (R * RECORD_BYTES + 8 if with_records else 0)
+                d2h = max(d2h, d2h_k + (N_ENV + 1) * 8 + NE * 5)
                 flush.zero_()
-            return sum(ms) / 1e3, recs, h2d, d2h
+            return wall, recs, h2d, d2h
 
         t_e2e, e2e_recs, h2d_b, d2h_b = e2e_loop(False)
+        check = self_check(ws_h, ev_host, host_seeds[K2 - 1].numpy())
         t_e2r, e2r_recs, _, d2h_rb = e2e_loop(True)
-        # ---- sizing run: k_label over 2^19 x 200-step episodes
-        sizing = label_sizing_run(L, core, lib, dev, stream, flush)
-        env_api = env_api_run(dev, stream)
-        c3 = c3_run(dev, stream, world, flush)
-        c5 = c5_run(dev, stream, world)
-        c4 = c4_run(dev, stream, world, flush)
-        lbf = label_batch_files_run() if rank == 0 else None
+        extras = {}
+        if not args.no_extras:
+            extras["c2_1024"] = c2_run(dev, stream, world, flush)
+            extras["c3"] = c3_run(dev, stream, world, flush)
+            extras["env_api"] = env_api_run(dev, stream)
+            extras["label_sizing"] = label_sizing_run(L, core, lib, dev, stream, flush)
+            extras["c5"] = c5_run(dev, stream, world)
+            extras["c4"] = c4_run(dev, stream, world, flush)
+            if rank == 0:
+                extras["label_batch_files"] = label_batch_files_run()
     clk = clocks.summary()
 
-    recs_per_step = nrec_log.sum(dim=1).to(torch.float64)
-    total_recs = float(recs_per_step.sum().item())
-    t_dev = sum(step_ms) / 1e3
-    t_syn = sum(synth_ms) / 1e3
-    tt = torch.tensor([t_dev, t_syn, t_e2e, t_e2r, total_recs, float(e2e_recs), float(e2r_recs)],
-                      dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = tt[:4].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt[4:].clone()
-        dist.all_reduce(sm)
-        t_dev, t_syn, t_e2e, t_e2r = mx.tolist()
-        total_recs, e2e_recs_all, e2r_recs_all = sm.tolist()
-    else:
-        e2e_recs_all, e2r_recs_all = float(e2e_recs), float(e2r_recs)
+    recs_k = nrec_log.sum(dim=1).to(torch.float64).cpu().numpy()
+    max_rec = float(nrec_log.max().item())
+    t_dev, t_syn, t_e2e, t_e2r, max_rec = max_over_ranks(
+        [sum(step_ms) / 1e3, sum(synth_ms) / 1e3, t_e2e, t_e2r, max_rec], world, dev)
+    total_recs, e2e_recs_all, e2r_recs_all = sum_over_ranks(
+        [float(recs_k.sum()), float(e2e_recs), float(e2r_recs)], world, dev)
     if rank != 0:
         dist.destroy_process_group()
         return
     hbm_peak, peak_src = peaks()
     recs_per_launch = total_recs / world / K
     alg_bytes = recs_per_launch * RECORD_BYTES + N_ENV * LABEL_BYTES
-    achieved = alg_bytes / (t_syn / K) / 1e9
-    traffic_b, traffic_recs = profile_traffic()
-    traffic = None
-    if traffic_b and traffic_recs:
-        traffic = traffic_b / traffic_recs * recs_per_launch
-    cb_sps, cb_eps, cb_sample = cpu_baseline(args.cpu_seconds)
+    step_s = t_syn / K
+    # latency roofline of the generator: the step cannot finish
+    # before the serial CPython seeding chain of the reset (1247 dependent
+    # steps, synth.py:103 -> init_by_array) plus the serial f64
+    # cum_robot_force recurrence of the longest episode (synth.py:192-196)
+    c_seed, c_cum, c_src = latency_constants()
+    sm_ghz = (clk.get("sm_mhz") or 1965.0) / 1e3
+    crit_cycles = 1247 * c_seed + max_rec * c_cum
+    floor_s = crit_cycles / (sm_ghz * 1e9)
+    prof = profile_json("r2_ncu_headline.json") or {}
     sps = total_recs / t_dev
+    cb_sps, cb_eps, cb_sample = cpu_baseline(args.cpu_seconds)
+    pyref = python_reference_baseline()
+    e2e_sps = e2e_recs_all / t_e2e
     out = {
         "metric": METRIC, "value": sps, "unit": "env-steps/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": 1e3 * t_dev / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "storage": "f32 records",
         "data": "synthetic",
         "trajectories_per_sec": N_ENV * world * K / t_dev,
-        "config": {"workload": WORKLOAD, "envs_per_gpu": N_ENV, "subtask": "Place",
-                   "fuzz_config": CFG, "mean_steps_per_episode": recs_per_launch / N_ENV,
-                   "parallelism": f"episodes sharded over {world} GPU(s), NCCL label all-gather",
-                   "l2": "flushed between timed steps (256 MiB write, excluded from timing)",
-                   "timing": "CUDA events per step on the launch stream, max over ranks",
-                   "step": "1 CUDA graph: tl_fuzz_ev (reset kernel + realize kernel that also emits the ordered event lists)"
-                           + (", then NCCL all_gather of labels + tl_mode_histogram of the gathered labels" if world > 1 else "")},
+        "config": bench_config(world),
+        "mean_steps_per_episode": recs_per_launch / N_ENV,
+        "step": "1 CUDA graph: tl_fuzz_ev (k_fuzz_reset + k_synth_cta, which also emits the ordered "
+                "event lists)" + (", NCCL all_gather of the labels + tl_mode_histogram of the "
+                                  "gathered labels" if world > 1 else ""),
+        "timing": "CUDA events per step on the launch stream, max over ranks",
         "gpu_launches": launches_per_step * K,
-        "roofline": {"kernel": "k_fuzz_reset + k_synth_cta (tl_fuzz_ev)", "bound": "hbm", "achieved": achieved,
-                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "avg_launch_ms": 1e3 * t_syn / K,
-                     "note": "93 B/record + 24 B/episode written; MT19937 + f64 generation is "
-                             "ALU/latency-bound, not HBM-bound (SURVEY 8(d))"},
-        "e2e": {"value": e2e_recs_all / t_e2e, "unit": "env-steps/s",
-                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
-                "steps": K2, "note": "C-ABI calls with host buffers: pinned host seeds -> GPU "
-                                      "(H2D copy), labels + ordered event lists written by the "
-                                      "kernels into pinned host memory (zero-copy D2H) every "
-                                      "step, one stream sync (records stay in HBM)",
+        "roofline": {
+            "kernel": "k_fuzz_reset + k_synth_cta (tl_fuzz_ev)", "bound": "latency",
+            "achieved": crit_cycles / step_s / 1e9, "peak": sm_ghz,
+            "unit": "GHz (critical-path cycles retired per second vs the SM clock)",
+            "frac": floor_s / step_s,
+            "floor_ms": 1e3 * floor_s, "avg_launch_ms": 1e3 * step_s,
+            "floor_model": (f"1247 seeding steps x {c_seed:.1f} cycles + longest episode "
+                            f"({int(max_rec)} records) x {c_cum:.1f} cycles of the f64 cum chain, at "
+                            f"the sampled SM clock; constants: {c_src}"),
+            "issue_active": prof.get("issue_active"), "warps_active": prof.get("warps_active"),
+            "traffic": prof.get("dram_bytes_per_launch"),
+            "profile": "profiles/r2_ncu_headline.json" if prof else None,
+            "hbm": {"achieved": alg_bytes / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": alg_bytes / step_s / 1e9 / hbm_peak, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "note": "93 B/record + 24 B/episode written; not the bound (MT19937 + f64 "
+                            "generation is latency-bound, SURVEY 8(d))"}},
+        "e2e": {"value": e2e_sps, "unit": "env-steps/s",
+                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": K2,
+                "timing": "time.perf_counter around the calls + stream synchronize, per step, "
+                          "max over ranks",
+                "note": "C-ABI tl_fuzz_ev with host buffers: pinned host seeds -> GPU (H2D), "
+                        "ordered event lists written by the kernel into pinned host memory "
+                        "(zero-copy), labels D2H (N>1: after the NCCL all-gather; histogram D2H)",
                 "with_records": {"value": e2r_recs_all / t_e2r, "unit": "env-steps/s",
                                  "d2h_bytes_per_step": d2h_rb,
-                                 "note": "same, plus tl_compact_records + D2H of every "
+                                 "note": "same, plus tl_scan_counts + tl_compact_records into one "
+                                         "contiguous staging buffer and ONE D2H copy of every "
                                          "generated record (93 B/env-step)"}},
-        "label_sizing": sizing,
-        "env_api": env_api,
-        "c3": c3,
-        "c5": c5,
-        "c4": c4,
-        "label_batch_files": lbf,
+        "self_check": check,
         "cpu_baseline": {"value": cb_sps, "unit": "env-steps/s", "cores": 1, "kind": "port",
                          "sample": cb_sample, "trajectories_per_sec": cb_eps,
                          "host": host_info()},
+        "python_reference": pyref,
         "clocks": clk,
     }
-    print(json.dumps(out))
+    pool = (pyref.get("pool") or {}).get("fuzz_and_label_sps") if isinstance(pyref, dict) else None
+    if pool:
+        out["vs_python_reference"] = {"e2e_ratio": e2e_sps / pool, "ratio": sps / pool,
+                                      "against": "python_reference.pool (all host cores)"}
+    out.update(extras)
+    print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()
 
