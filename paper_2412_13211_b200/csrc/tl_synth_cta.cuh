@@ -65,6 +65,7 @@ struct CtaSmem {
   uint8_t sflag[kSteps];
   int32_t misc[16];
   int32_t red[8];
+  int32_t tk[2];            // claimed episode tickets (double-buffered by iteration)
   tl_cset cs;
   // the CTA's next episode, copied in by cp.async while this one runs
   alignas(16) uint32_t mt_pf[kMtN];
@@ -156,14 +157,21 @@ __device__ __forceinline__ int block_max(int v, int32_t* red) {
 
 // ---- fused event lists ---------------------------------------------------------
 // Episode e publishes its event count as soon as its label is final
-// (aggregate flag); after its episode loop each CTA resolves the exclusive
-// prefix of its episodes by a warp-wide decoupled look-back over the
-// predecessors' statuses (aggregate or inclusive prefix), publishes the
-// inclusive prefix and writes the ordered (kind, t) list from the step
-// masks it wrote -- events.py:109-191 without a separate scan kernel.
-// Waits only ever target lower episode indices whose aggregates are
-// published without waiting, so the look-back cannot deadlock.
+// (aggregate flag, after a release fence); once every episode has been
+// claimed, CTAs take episodes again by a second ticket, in index order, and
+// resolve each one's exclusive prefix by a warp-wide decoupled look-back over
+// the predecessors' statuses (aggregate or inclusive prefix), publish the
+// inclusive prefix and write the ordered (kind, t) list from the step masks
+// -- events.py:109-191 without a separate scan kernel.
+// Progress: an emission ticket is only handed out after the last episode
+// ticket, so every episode a look-back waits on was claimed by a CTA that was
+// running when it claimed it, and that CTA publishes the aggregate without
+// waiting on anything.  No assumption that the whole grid is co-resident
+// (concurrent kernels, MPS or green-context SM limits cannot hang it).
+// Waiting warps back off with __nanosleep so they do not take issue slots
+// from the CTAs still realizing episodes on the same SM.
 __device__ __forceinline__ void ev_publish_agg(const SynthParams& p, int e, int n_ev) {
+  __threadfence();  // the episode's step masks / n_rec before its flag
   atomicExch(&p.ev_state[e], kTileAgg | (unsigned long long)n_ev);
 }
 
@@ -172,6 +180,7 @@ __device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
   volatile unsigned long long* st = p.ev_state;
   int64_t prefix = 0;
   int j = e - 1;
+  unsigned ns = 64;
   while (j >= 0) {
     const int idx = j - lane;
     const unsigned long long v = idx >= 0 ? st[idx] : kTilePrefix;
@@ -180,7 +189,11 @@ __device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
     const unsigned zm = __ballot_sync(kFull, flag == 0);
     const int lim = pm ? __ffs(pm) - 1 : 31;             // lanes 0..lim are needed
     const unsigned need = lim == 31 ? kFull : ((2u << lim) - 1u);
-    if (zm & need) continue;                              // a predecessor is not published yet
+    if (zm & need) {                                      // a predecessor is not published yet
+      __nanosleep(ns);
+      ns = min(ns * 2, 2048u);
+      continue;
+    }
     int64_t c = lane <= lim ? (int64_t)(v & kTileValMask) : 0;
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
@@ -191,12 +204,23 @@ __device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
   return prefix;
 }
 
+// warp 0 of every CTA, after its episode loop (all episodes claimed)
 template <int DOFMAX>
 __device__ void ev_emit_all(const SynthParams& p) {
   const int lane = lane_id();
-  for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
-    // this episode's own aggregate (the labels may live in host memory)
-    const int n_ev = (int)(((volatile unsigned long long*)p.ev_state)[e] & kTileValMask);
+  volatile unsigned long long* st = p.ev_state;
+  for (;;) {
+    int e = 0;
+    if (lane == 0) e = (int)atomicAdd(&p.tickets[1], 1u);
+    e = __shfl_sync(kFull, e, 0);
+    if (e >= p.n_env) break;
+    // the episode's own aggregate (published by whichever CTA realized it)
+    unsigned long long v = st[e];
+    for (unsigned ns = 64; (v & ~kTileValMask) == 0; ns = min(ns * 2, 2048u)) {
+      __nanosleep(ns);
+      v = st[e];
+    }
+    const int n_ev = (int)(v & kTileValMask);
     const int64_t prefix = ev_lookback(p, e);
     if (lane == 0) {
       atomicExch(&p.ev_state[e], kTilePrefix | (unsigned long long)(prefix + n_ev));
@@ -204,13 +228,14 @@ __device__ void ev_emit_all(const SynthParams& p) {
       if (e == p.n_env - 1) p.ev_off[p.n_env] = prefix + n_ev;
     }
     if (n_ev == 0) continue;
+    __threadfence();  // acquire: the step masks of another CTA's episode
     const int sub = p.fuzz_subtask;  // fused event lists are a fuzz (single-subtask) path
-    const int64_t rs = p.out.rec_start[e];
-    const int n = p.out.n_rec[e];
+    const int64_t rs = __ldcg(&p.out.rec_start[e]);
+    const int n = __ldcg(&p.out.n_rec[e]);
     int64_t base = prefix;
     for (int t0 = 0; t0 < n; t0 += 32) {
       const int t = t0 + lane;
-      const uint32_t mask = t < n ? p.step_mask[rs + t] : 0u;
+      const uint32_t mask = t < n ? __ldcg(&p.step_mask[rs + t]) : 0u;
       const int cnt = __popc(mask);
       const int incl = warp_incl_scan(cnt);
       int64_t pos = base + incl - cnt;
@@ -243,7 +268,14 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
 
   int wave_no = 0;
   bool pf = false;  // the next episode's inputs are in flight to S.*_pf
-  for (int e = blockIdx.x; e < p.n_env; e += gridDim.x) {
+  // episodes by ticket, in claim order (dynamic load balance across CTAs);
+  // the next episode is claimed at the top of the current one so its inputs
+  // can be prefetched, parity-buffered in S.tk (>= 1 barrier per iteration)
+  if (tid == 0) S.tk[0] = (int)atomicAdd(&p.tickets[0], 1u);
+  __syncthreads();
+  int e = S.tk[0];
+  for (int it = 1; e < p.n_env; it++) {
+    if (tid == 0) S.tk[it & 1] = (int)atomicAdd(&p.tickets[0], 1u);
     if (tid == 0 && e == 0) TL_STAMP(10);
     // ---------------- script + seeded RNG state -------------------------------
     tl_script sc;
@@ -275,6 +307,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
         if (p.ev_off) ev_publish_agg(p, e, 0);
       }
       __syncthreads();
+      e = S.tk[it & 1];
       continue;
     }
     const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
@@ -282,8 +315,8 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     RzConst z;
     const int st0 = realizer_init(z, sc, p.th, dof);
     __syncthreads();
+    const int en = S.tk[it & 1];
     {  // S.*_pf are free again (copied out above): fetch the next episode's inputs
-      const int en = e + gridDim.x;
       if (en < p.n_env) {
         const uint32_t* src = p.states + (int64_t)en * kMtN;
         for (int i = tid; i < kMtN / 4; i += kCtaThreads) cp_async16(S.mt_pf + 4 * i, src + 4 * i);
@@ -314,6 +347,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     if (st0 != TL_OK) {
       fail(st0, -1);
       __syncthreads();
+      e = en;
       continue;
     }
     if (tid == 0 && e == 0) TL_STAMP(11);
@@ -670,6 +704,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     __syncthreads();
     if (tid == 0 && e == 0) TL_STAMP(13);
     if (tid == 0 && e == gridDim.x) TL_STAMP(14);
+    e = en;
   }
   if (p.ev_off && warp == 0) ev_emit_all<DOFMAX>(p);
 }

@@ -15,24 +15,24 @@ __global__ void k(uint32_t* mt_out, double* cum_out, const double* u, long long*
   const uint32_t key = 0x12345678u;
   __syncwarp();
   long long t0 = clock64();
-  // init_by_array, key length 1: first loop (max(624, 1) steps), second loop 623
+  // init_by_array, key length 1: first loop (max(624, 1) steps), second loop
+  // 623.  The old word mt[i] does not depend on the chain: it is generated
+  // off the critical path (k_fuzz_reset prefetches it a group ahead), so only
+  // the shift / xor / multiply / xor / add on the previous word is timed.
   uint32_t prev = mt[0];
-  int i = 1;
-#pragma unroll 1
-  for (int k = 624; k; k--) {
-    const uint32_t v = (mt[i] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
-    mt[i] = v;
+#pragma unroll 4
+  for (int i = 1; i < 625; i++) {
+    const uint32_t old = 19650218u + (uint32_t)i * 2654435761u;
+    const uint32_t v = (old ^ ((prev ^ (prev >> 30)) * 1664525u)) + key;
+    mt[i % 624] = v;
     prev = v;
-    i++;
-    if (i >= 624) { mt[0] = mt[623]; i = 1; }
   }
-#pragma unroll 1
-  for (int k = 623; k; k--) {
-    const uint32_t v = (mt[i] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
+#pragma unroll 4
+  for (int i = 1; i < 624; i++) {
+    const uint32_t old = 40503u + (uint32_t)i * 2246822519u;
+    const uint32_t v = (old ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
     mt[i] = v;
     prev = v;
-    i++;
-    if (i >= 624) { mt[0] = mt[623]; i = 1; }
   }
   long long t1 = clock64();
   double cum = 0.0;
