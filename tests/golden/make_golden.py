@@ -505,15 +505,18 @@ def make_classify():
 
 # -- filter cases -------------------------------------------------------------------
 
-def make_filter():
-    rng = random.Random(9)
+def make_filter(dup=False):
+    """dup=True: episode_ids drawn WITH replacement (the same episode in
+    several files), so manifest tie order is pinned too (pipeline.py:329)."""
+    rng = random.Random(11 if dup else 9)
     cases = []
-    for i in range(100):
+    for i in range(60 if dup else 100):
         n = rng.choice([0, 5, 50, 300, 1200])
         targets = [f"obj-{c}" for c in "ABCD"[:rng.choice([1, 2, 4])]]
         tasks = ["TidyHouse", "SetTable", "Custom"]
         labels = []
-        ids = rng.sample(range(10 * n + 10), n)
+        ids = ([rng.randrange(max(1, n // 4)) for _ in range(n)] if dup
+               else rng.sample(range(10 * n + 10), n))
         for j in range(n):
             kind = rng.choice(KINDS)
             mode = rng.choice(MODE_IDS[kind])
@@ -549,13 +552,18 @@ def make_filter():
                       "counts": md["counts"], "shortfalls": md["shortfalls"],
                       "manifest_sha256": __import__("hashlib").sha256(
                           man.to_json().encode()).hexdigest()})
-    with gzip.open(os.path.join(OUT, "filter.json.gz"), "wt") as f:
+    name = "filter_dup.json.gz" if dup else "filter.json.gz"
+    with gzip.open(os.path.join(OUT, name), "wt") as f:
         json.dump(cases, f)
+
+
+def make_filter_dup():
+    make_filter(dup=True)
 
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["fuzz", "defining", "long", "crafted", "scripts",
-                             "classify", "filter"]
+                             "classify", "filter", "filter_dup"]
     for w in which:
         globals()["make_" + w]()
         print("wrote", w)

@@ -273,6 +273,28 @@ def test_filter_semantics():
     assert len(m.entries) == 15 and len(m.shortfalls) == 1
 
 
+@pytest.mark.parametrize("name", ["filter", "filter_dup"])
+def test_filter_manifest_bytes_vs_reference(name):
+    """filter_labels over the reference fixtures: the manifest JSON is
+    byte-identical (sha256) to the reference's, including the entry order
+    among repeated episode_ids (filter_dup: ids drawn with replacement;
+    reference pipeline.py:299-329 emits pool by pool, then stable-sorts)."""
+    import hashlib
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from golden_data import js
+    for case in js(name):
+        labels = [T.LabelRecord(episode_id=eid, subtask=sub, mode_id=mode,
+                                success_once=mode.split(".")[1].startswith("s"),
+                                success_at_end=False, target_id=tgt, task=task,
+                                split="Train", policy_tag="RL", source=src)
+                  for eid, sub, mode, tgt, task, src in case["labels"]]
+        man = T.filter_labels(labels, T.FilterSpec.from_dict(case["spec"]))
+        assert [e.episode_id for e in man.entries] == case["selected"]
+        assert hashlib.sha256(man.to_json().encode()).hexdigest() == case["manifest_sha256"]
+
+
 def test_c5_device_filter_matches_host_filter():
     """C5 shape at small scale: device bucket encoding + selection + counts
     == filter_labels over the equivalent LabelRecords (host buckets, pinned
