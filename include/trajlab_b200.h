@@ -25,6 +25,8 @@
  *   tl_filter_select   filter_labels selection (pipeline.py:276-338)
  *   tl_mode_histogram  mode counting of label_batch/mode_table
  *                      (pipeline.py:148-150, analytics.py:140-158)
+ *   tl_validate_records validate / check_valid per-record invariants
+ *                      (model.py:232-288)
  */
 #ifndef TRAJLAB_B200_H
 #define TRAJLAB_B200_H
@@ -367,6 +369,38 @@ int tl_scan_counts(const int32_t* counts, int32_t n, int64_t* off,
  * batch: dst->planes/grasped at dst_start[e]; writes dst->rec_start/n_rec. */
 int tl_compact_records(const tl_records* src, int32_t n_env,
                        const int64_t* dst_start, tl_records* dst, void* stream);
+
+/* ---- structural validation (model.py:232-281 validate / check_valid) ----
+ * Per-record invariant codes over a record batch.  dof may be 0 when only
+ * the 9 scalar planes are present (validation reads dist_ee_rest,
+ * dist_obj_goal, force_ee_target, cum_robot_force, art_q).  t (optional,
+ * per record, same indexing as the planes): the stored step index, checked
+ * against the record's position; NULL = implicit t.  vb[e]: the episode's
+ * articulation (has_art = articulation_kind != None) and f64 bounds.
+ * vflags[r] (optional) = TL_VF_* bits; vsum[e] = counts of records with an
+ * error bit / the warning bit, the first flagged index (-1 if none) and
+ * n_rec < 2.  Header checks (arm_dof, rest_arm length, bounds order,
+ * Open/Close without articulation) are host-side: they need no records. */
+enum {
+  TL_VF_T_MISMATCH = 1,     /* "record i has step index t=.., expected i" */
+  TL_VF_ARM_LENGTH = 2,     /* host objects only: arm vectors vs arm_dof   */
+  TL_VF_CUM_INVALID = 4,    /* "cumulative force invalid at t=i: v"        */
+  TL_VF_CUM_DECREASED = 8,  /* "cumulative force decreased at t=i"         */
+  TL_VF_DEE_INVALID = 16,   /* "dist_ee_rest invalid at t=i: v"            */
+  TL_VF_DOG_NEGATIVE = 32,  /* "dist_obj_goal negative at t=i: v"          */
+  TL_VF_FET_NEGATIVE = 64,  /* "force_ee_target negative at t=i: v"        */
+  TL_VF_ART_RANGE = 128     /* warning "art_q out of [qmin, qmax] at t=i"  */
+};
+typedef struct tl_vbounds {
+  double art_qmin, art_qmax;
+  int32_t has_art, pad;
+} tl_vbounds;
+typedef struct tl_vsummary {
+  int32_t n_error_records, n_warning_records, first_flagged, too_short;
+} tl_vsummary;
+int tl_validate_records(const tl_records* recs, int32_t n_env, const tl_vbounds* vb,
+                        const int64_t* t, uint8_t* vflags, tl_vsummary* vsum,
+                        void* stream);
 
 /* K6: counts per global mode id (status==0 only); hist[39] int64, zeroed
  * by the call. */

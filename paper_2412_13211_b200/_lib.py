@@ -103,6 +103,13 @@ SCRIPT_DTYPE = np.dtype([("step_off", "<i8"), ("seed", "<i8"),
                          ("initial_level", "<i4"), ("initial_grasped", "<i4"),
                          ("initial_contact", "<i4"), ("arm_dof", "<i4"),
                          ("initial_dist_obj_goal", "<f8")])
+VBOUNDS_DTYPE = np.dtype([("art_qmin", "<f8"), ("art_qmax", "<f8"), ("has_art", "<i4"),
+                          ("pad", "<i4")])
+VSUMMARY_DTYPE = np.dtype([("n_error_records", "<i4"), ("n_warning_records", "<i4"),
+                           ("first_flagged", "<i4"), ("too_short", "<i4")])
+# tl_validate_records per-record codes (TL_VF_*)
+VF_T_MISMATCH, VF_ARM_LENGTH, VF_CUM_INVALID, VF_CUM_DECREASED = 1, 2, 4, 8
+VF_DEE_INVALID, VF_DOG_NEGATIVE, VF_FET_NEGATIVE, VF_ART_RANGE = 16, 32, 64, 128
 assert LABEL_DTYPE.itemsize == 24 and SCRIPT_DTYPE.itemsize == 56
 CSET_BYTES = ctypes.sizeof(Cset_c)
 
@@ -175,6 +182,7 @@ def lib():
         "tl_filter_buckets": ([vp, vp, i64, vp, vp, vp, i32, vp, vp], ctypes.c_int),
         "tl_allgather_labels": ([vp, vp, i64, vp, vp], ctypes.c_int),
         "tl_allreduce_counts": ([vp, vp, i64, vp], ctypes.c_int),
+        "tl_validate_records": ([P(Records_c), i32, vp, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -196,7 +204,7 @@ def exported_symbols():
             "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
             "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions",
             "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets", "tl_fuzz_ev",
-            "tl_allgather_labels", "tl_allreduce_counts"]
+            "tl_allgather_labels", "tl_allreduce_counts", "tl_validate_records"]
 
 
 def check(rc, what):

@@ -485,3 +485,18 @@ def filter_select(bucket, n_buckets, pool_b0, bucket_w, quota):
                                   L.ptr(scratch), L.stream_ptr())
     L.check(rc, "tl_filter_select")
     return sel[:n], ps[:n_pools]
+
+
+def validate_records(rb: RecordBatch, vbounds, t=None):
+    """tl_validate_records (model.py:255-274 invariants as TL_VF_* codes):
+    -> (vflags u8 device tensor per record, per-episode tl_vsummary numpy)."""
+    torch = _torch()
+    dev = rb.planes.device
+    n = rb.n_env
+    vflags = torch.zeros(max(int(rb.planes.shape[1]), 1), dtype=torch.uint8, device=dev)
+    vsum = torch.empty(max(n, 1) * L.VSUMMARY_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    vb = torch.from_numpy(np.ascontiguousarray(vbounds).view(np.uint8).copy()).to(dev)
+    rc = L.lib().tl_validate_records(ctypes.byref(rb.c()), n, L.ptr(vb), L.ptr(t), L.ptr(vflags),
+                                     L.ptr(vsum), L.stream_ptr())
+    L.check(rc, "tl_validate_records")
+    return vflags, vsum.cpu().numpy().view(L.VSUMMARY_DTYPE)[:n]

@@ -19,6 +19,7 @@
 #include "tl_filter.cuh"
 #include "tl_env.cuh"
 #include "tl_analytics.cuh"
+#include "tl_validate.cuh"
 
 namespace {
 
@@ -821,6 +822,21 @@ int tl_prof_read(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tl_prof, sizeof(unsigned long long) * 128) == cudaSuccess ? 0 : TL_E_CUDA;
 }
 #endif
+
+int tl_validate_records(const tl_records* recs, int32_t n_env, const tl_vbounds* vb,
+                        const int64_t* t, uint8_t* vflags, tl_vsummary* vsum, void* stream) {
+  if (!recs || n_env < 0 || recs->dof < 0 || recs->dof > TL_MAX_DOF || recs->dtype < 0 ||
+      recs->dtype > 1)
+    return TL_E_INVALID;
+  if (n_env == 0) return TL_OK;
+  if (!vb || !vsum || !recs->planes || !recs->rec_start || !recs->n_rec) return TL_E_INVALID;
+  const int grid = blocks_for(n_env, kValidateWarps, sm_count() * 16);
+  if (recs->dtype == 0)
+    k_validate<float><<<grid, kValidateWarps * 32, 0, S(stream)>>>(*recs, n_env, vb, t, vflags, vsum);
+  else
+    k_validate<double><<<grid, kValidateWarps * 32, 0, S(stream)>>>(*recs, n_env, vb, t, vflags, vsum);
+  return check_launch();
+}
 
 int tl_mode_histogram(const tl_label* labels, int32_t n, int64_t* hist, void* stream) {
   if (!hist || n < 0 || (n > 0 && !labels)) return TL_E_INVALID;

@@ -95,6 +95,7 @@ def test_labelrecord_json_is_sort_keys_canonical():
     assert LabelRecord.from_dict(d) == r
 
 
+@pytest.mark.gpu  # the writers run check_valid, i.e. k_validate
 def test_trjl_roundtrip_bit_exact():
     from paper_2412_13211_b200 import io_binary as B
     from paper_2412_13211_b200.model import TimestepRecord, Trajectory, TrajectoryHeader

@@ -22,6 +22,7 @@ def _same_record(a, b):
             assert x == y, f
 
 
+@pytest.mark.gpu  # the writers run check_valid, i.e. k_validate
 def test_binary_reader_writer_byte_identical():
     g = js("io")
     for c in g["cases"]:
