@@ -241,7 +241,10 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off,
  * e*cap_per_env (rec_start and n_rec written).  label_csets (device) is
  * indexed [subtask*3 + articulation kind] (0 none, 1 fridge, 2 drawer).
  * script_kind/script_gap/scripts (optional) receive the sampled scripts
- * (steps at e*(cfg.max_events+4)); scratch >= tl_fuzz_scratch_bytes().   */
+ * (steps at e*(cfg.max_events+4)); scratch >= tl_fuzz_scratch_bytes(),
+ * zero-filled before its first use (every call leaves its claim counters at
+ * zero again).  Episodes are realized longest-first (length buckets filled
+ * by the reset kernel) when cap_per_env > 64; results do not depend on it. */
 size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg /* host */);
 int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask,
             const tl_fuzz_cfg* cfg /* host */,

@@ -370,7 +370,8 @@ class SynthWorkspace:
         self.script_kind = torch.empty(n_env * max_steps, dtype=torch.uint8, device=dev) if with_scripts else None
         self.script_gap = torch.empty(n_env * max_steps, dtype=torch.int32, device=dev) if with_scripts else None
         c_cfg = L.FuzzCfg_c(max_steps - 4, 1, 1, 0, 1.0, 0.5)
-        self.scratch = torch.empty(int(L.lib().tl_fuzz_scratch_bytes(n_env, ctypes.byref(c_cfg))),
+        # zero-filled once: the claim counters in it are left at zero by every call
+        self.scratch = torch.zeros(int(L.lib().tl_fuzz_scratch_bytes(n_env, ctypes.byref(c_cfg))),
                                    dtype=torch.uint8, device=dev)
         self.n_env, self.cap, self.dof, self.max_steps = n_env, cap_per_env, dof, max_steps
 

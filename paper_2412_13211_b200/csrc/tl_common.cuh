@@ -319,6 +319,12 @@ __device__ __forceinline__ double uniform_rn(double a, double b, double r) {
 }
 
 // warp inclusive scan (int)
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int warp_incl_scan(int v) {
   const int lane = lane_id();
 #pragma unroll

@@ -64,13 +64,41 @@ struct SynthParams {
   int64_t* ev_off;
   uint8_t* ev_kind;
   int32_t* ev_t;
-  unsigned long long* ev_state;  // [n_env] look-back status, zeroed per launch
-  // [2] claim counters (episodes, event-list emission), zeroed by the reset
-  // kernel: k_synth_cta takes episodes by ticket, so every cross-CTA wait
-  // targets an episode already claimed by a running CTA (no co-residency
-  // assumption, see ev_emit_all)
+  unsigned long long* ev_state;  // [n_env/32] block look-back status, zeroed per launch
+  unsigned int* ev_blk_done;     // [n_env/32] realized episodes per block, zeroed per launch
+  // claim counters: [0] episodes, [1] event-list offset blocks,
+  // [kTkEmit] event-list writing (zeroed by the reset kernel),
+  // [2] exited CTAs, [4 + b] episodes in length bucket b (left
+  // at zero by every k_synth_cta launch; zero-filled scratch before the first).
+  // k_synth_cta takes episodes by ticket, so every cross-CTA wait targets an
+  // episode already claimed by a running CTA (no co-residency assumption,
+  // see ev_emit_all)
   unsigned int* tickets;
+  // longest-first episode order (fuzz, long-episode configs): bucket b holds
+  // the episodes of b+1 64-record waves (b = 15: 16 or more) at
+  // order[b * n_env + slot], filled by k_fuzz_reset; null = index order
+  int32_t* order;
 };
+
+constexpr int kLenBuckets = 16;
+constexpr int kTkBucket = 4;  // tickets[kTkBucket + b]
+constexpr int kTkEmit = kTkBucket + kLenBuckets;  // event-list writing claims
+
+// ticket -> episode: tickets walk the length buckets from the longest down
+// (LPT order: a long episode claimed last would otherwise set the batch
+// time, synth.py run lengths vary ~4x around the mean)
+__device__ __forceinline__ int claim_episode(const SynthParams& p) {
+  const int t = (int)atomicAdd(&p.tickets[0], 1u);
+  if (p.order == nullptr || t >= p.n_env) return t;
+  int r = t;
+#pragma unroll 1
+  for (int b = kLenBuckets - 1; b >= 0; b--) {
+    const int c = (int)__ldcg(&p.tickets[kTkBucket + b]);
+    if (r < c) return __ldcg(&p.order[(int64_t)b * p.n_env + r]);
+    r -= c;
+  }
+  return p.n_env;  // unreachable: the buckets hold every episode
+}
 
 __device__ __forceinline__ bool in_alpha(int k, int ev) {
 #pragma unroll
@@ -388,7 +416,11 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
                          : rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
   const int ms = p.cfg.max_events + 4;
   if (lane == 0) TL_STAMP(0);
-  if (blockIdx.x == 0 && lane == 0 && p.tickets) { p.tickets[0] = 0u; p.tickets[1] = 0u; }
+  if (blockIdx.x == 0 && lane == 0 && p.tickets) {
+    p.tickets[0] = 0u;  // episode claims
+    p.tickets[1] = 0u;  // event-list block claims
+    p.tickets[kTkEmit] = 0u;
+  }
   if (valid) {
     const int64_t seed = p.seeds[e];
     // odd lanes: realize RNG, final state written straight to global memory
@@ -416,7 +448,15 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
       t.seed = seed ^ 0x5EED;
       t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
       p.scripts[e] = t;
-      if (p.ev_off) p.ev_state[e] = 0ull;  // event look-back status of this launch
+      if (p.order) {  // length bucket for the realize kernel's longest-first claims
+        const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / 64);
+        const unsigned slot = atomicAdd(&p.tickets[kTkBucket + b], 1u);
+        p.order[(int64_t)b * p.n_env + slot] = (int32_t)e;
+      }
+      if (p.ev_off && (e << 5) < p.n_env) {  // event-list block state of this launch
+        p.ev_state[e] = 0ull;
+        p.ev_blk_done[e] = 0u;
+      }
       if (p.out.rec_start) {  // record layout (tl_fuzz); the env reset has none
         p.out.rec_start[e] = e * p.cap_per_env;
         p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;
@@ -430,7 +470,9 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
 // streamed straight to global memory: no shared memory)
 __global__ void __launch_bounds__(128) k_seed_states(SynthParams p) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e == 0 && p.tickets) { p.tickets[0] = 0u; p.tickets[1] = 0u; }
+  if (e == 0 && p.tickets) {
+    p.tickets[0] = 0u; p.tickets[1] = 0u; p.tickets[kTkEmit] = 0u;
+  }
   if (e < p.n_env) mt_seed_lane_stream(p.scripts[e].seed, p.states + e * kMtN);
 }
 

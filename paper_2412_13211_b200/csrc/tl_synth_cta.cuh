@@ -156,31 +156,29 @@ __device__ __forceinline__ int block_max(int v, int32_t* red) {
 }
 
 // ---- fused event lists ---------------------------------------------------------
-// Episode e publishes its event count as soon as its label is final
-// (aggregate flag, after a release fence); once every episode has been
-// claimed, CTAs take episodes again by a second ticket, in index order, and
-// resolve each one's exclusive prefix by a warp-wide decoupled look-back over
-// the predecessors' statuses (aggregate or inclusive prefix), publish the
-// inclusive prefix and write the ordered (kind, t) list from the step masks
-// -- events.py:109-191 without a separate scan kernel.
-// Progress: an emission ticket is only handed out after the last episode
-// ticket, so every episode a look-back waits on was claimed by a CTA that was
-// running when it claimed it, and that CTA publishes the aggregate without
-// waiting on anything.  No assumption that the whole grid is co-resident
-// (concurrent kernels, MPS or green-context SM limits cannot hang it).
-// Waiting warps back off with __nanosleep so they do not take issue slots
-// from the CTAs still realizing episodes on the same SM.
-__device__ __forceinline__ void ev_publish_agg(const SynthParams& p, int e, int n_ev) {
-  __threadfence();  // the episode's step masks / n_rec before its flag
-  atomicExch(&p.ev_state[e], kTileAgg | (unsigned long long)n_ev);
+// events.py:109-191 without a separate scan kernel.  A CTA that finishes an
+// episode (label written) counts it in its 32-episode block's counter
+// (release: fence, then the atomic).  Once a CTA's episode claims are
+// exhausted, its warps take blocks by a second ticket, each once the block's
+// 32 episodes are realized (one acquire load per back-off interval, no
+// per-episode spinning while other CTAs on the SM still realize): warp scan
+// of the 32 labels' n_events, a decoupled look-back over the preceding
+// blocks' statuses (aggregate or inclusive prefix, ev_state[block]), ev_off;
+// then the ordered (kind, t) lists from the step masks, an episode per claim.
+// Progress: the wait targets episodes that were all claimed by CTAs that
+// were running when they claimed them, and realizing an episode waits on
+// nothing -- no assumption that the whole grid is co-resident (concurrent
+// kernels, MPS or green-context SM limits cannot hang it).
+__device__ __forceinline__ void ev_mark_realized(const SynthParams& p, int e) {
+  __threadfence();  // the episode's label, step masks and n_rec before the count
+  atomicAdd(&p.ev_blk_done[e >> 5], 1u);
 }
 
-__device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
+__device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int blk) {
   const int lane = lane_id();
   volatile unsigned long long* st = p.ev_state;
   int64_t prefix = 0;
-  int j = e - 1;
-  unsigned ns = 64;
+  int j = blk - 1;
   while (j >= 0) {
     const int idx = j - lane;
     const unsigned long long v = idx >= 0 ? st[idx] : kTilePrefix;
@@ -189,9 +187,8 @@ __device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
     const unsigned zm = __ballot_sync(kFull, flag == 0);
     const int lim = pm ? __ffs(pm) - 1 : 31;             // lanes 0..lim are needed
     const unsigned need = lim == 31 ? kFull : ((2u << lim) - 1u);
-    if (zm & need) {                                      // a predecessor is not published yet
-      __nanosleep(ns);
-      ns = min(ns * 2, 2048u);
+    if (zm & need) {                                      // a predecessor block not published yet
+      __nanosleep(32);
       continue;
     }
     int64_t c = lane <= lim ? (int64_t)(v & kTileValMask) : 0;
@@ -204,41 +201,60 @@ __device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int e) {
   return prefix;
 }
 
-// warp 0 of every CTA, after its episode loop (all episodes claimed)
+// every warp of every CTA, after its episode loop (all episodes claimed):
+// phase A resolves ev_off by 32-episode blocks (each once its episodes are
+// realized), phase B writes one episode's list per warp claim (all warps of
+// the finished CTAs share the writing)
 template <int DOFMAX>
 __device__ void ev_emit_all(const SynthParams& p) {
   const int lane = lane_id();
+  const int n_blk = (p.n_env + 31) / 32;
+  for (;;) {  // phase A: offsets, a block as soon as its 32 episodes are realized
+    int blk = 0;
+    if (lane == 0) {
+      blk = (int)atomicAdd(&p.tickets[1], 1u);
+      const unsigned want = (unsigned)min(32, p.n_env - blk * 32);
+      for (unsigned ns = 64; blk < n_blk && ld_acquire_u32(&p.ev_blk_done[blk]) < want;
+           ns = min(ns * 2, 256u))
+        __nanosleep(ns);
+    }
+    blk = __shfl_sync(kFull, blk, 0);
+    if (blk >= n_blk) break;
+    __threadfence();
+    const int e = blk * 32 + lane;
+    const int n_ev = e < p.n_env ? __ldcg(&p.labels[e].n_events) : 0;  // 0 for failed episodes
+    const int incl = warp_incl_scan(n_ev);
+    const int total = __shfl_sync(kFull, incl, 31);
+    if (lane == 0) atomicExch(&p.ev_state[blk], kTileAgg | (unsigned long long)total);
+    const int64_t prefix = ev_lookback(p, blk);
+    const int64_t my_off = prefix + incl - n_ev;
+    if (e < p.n_env) p.ev_off[e] = my_off;
+    if (e == p.n_env - 1) p.ev_off[p.n_env] = my_off + n_ev;
+    __threadfence();  // the block's ev_off before its inclusive-prefix status
+    __syncwarp();
+    if (lane == 0) atomicExch(&p.ev_state[blk], kTilePrefix | (unsigned long long)(prefix + total));
+  }
+  const int sub = p.fuzz_subtask;  // fused event lists are a fuzz (single-subtask) path
   volatile unsigned long long* st = p.ev_state;
-  for (;;) {
+  for (;;) {  // phase B: lists
     int e = 0;
-    if (lane == 0) e = (int)atomicAdd(&p.tickets[1], 1u);
+    if (lane == 0) e = (int)atomicAdd(&p.tickets[kTkEmit], 1u);
     e = __shfl_sync(kFull, e, 0);
     if (e >= p.n_env) break;
-    // the episode's own aggregate (published by whichever CTA realized it)
-    unsigned long long v = st[e];
-    for (unsigned ns = 64; (v & ~kTileValMask) == 0; ns = min(ns * 2, 2048u)) {
-      __nanosleep(ns);
-      v = st[e];
-    }
-    const int n_ev = (int)(v & kTileValMask);
-    const int64_t prefix = ev_lookback(p, e);
-    if (lane == 0) {
-      atomicExch(&p.ev_state[e], kTilePrefix | (unsigned long long)(prefix + n_ev));
-      p.ev_off[e] = prefix;
-      if (e == p.n_env - 1) p.ev_off[p.n_env] = prefix + n_ev;
-    }
-    if (n_ev == 0) continue;
-    __threadfence();  // acquire: the step masks of another CTA's episode
-    const int sub = p.fuzz_subtask;  // fused event lists are a fuzz (single-subtask) path
+    // the block's inclusive prefix is published after its episodes were realized
+    // and its ev_off written: only then are the label and the offsets final
+    while ((st[e >> 5] & ~kTileValMask) != kTilePrefix) __nanosleep(64);
+    __threadfence();
+    if (__ldcg(&p.labels[e].n_events) == 0) continue;
+    int64_t base = __ldcg(&p.ev_off[e]);
     const int64_t rs = __ldcg(&p.out.rec_start[e]);
     const int n = __ldcg(&p.out.n_rec[e]);
-    int64_t base = prefix;
     for (int t0 = 0; t0 < n; t0 += 32) {
       const int t = t0 + lane;
       const uint32_t mask = t < n ? __ldcg(&p.step_mask[rs + t]) : 0u;
       const int cnt = __popc(mask);
-      const int incl = warp_incl_scan(cnt);
-      int64_t pos = base + incl - cnt;
+      const int inc = warp_incl_scan(cnt);
+      int64_t pos = base + inc - cnt;
       uint32_t m = mask;
       while (m) {
         const int k = __ffs(m) - 1;
@@ -247,7 +263,7 @@ __device__ void ev_emit_all(const SynthParams& p) {
         p.ev_t[pos] = t;
         pos++;
       }
-      base += __shfl_sync(kFull, incl, 31);
+      base += __shfl_sync(kFull, inc, 31);
     }
   }
 }
@@ -271,11 +287,11 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
   // episodes by ticket, in claim order (dynamic load balance across CTAs);
   // the next episode is claimed at the top of the current one so its inputs
   // can be prefetched, parity-buffered in S.tk (>= 1 barrier per iteration)
-  if (tid == 0) S.tk[0] = (int)atomicAdd(&p.tickets[0], 1u);
+  if (tid == 0) S.tk[0] = claim_episode(p);
   __syncthreads();
   int e = S.tk[0];
   for (int it = 1; e < p.n_env; it++) {
-    if (tid == 0) S.tk[it & 1] = (int)atomicAdd(&p.tickets[0], 1u);
+    if (tid == 0) S.tk[it & 1] = claim_episode(p);
     if (tid == 0 && e == 0) TL_STAMP(10);
     // ---------------- script + seeded RNG state -------------------------------
     tl_script sc;
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
         L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;
-        if (p.ev_off) ev_publish_agg(p, e, 0);
+        if (p.ev_off) ev_mark_realized(p, e);
       }
       __syncthreads();
       e = S.tk[it & 1];
@@ -341,7 +357,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;
         if (FUZZ) p.out.n_rec[e] = 0;
-        if (p.ev_off) ev_publish_agg(p, e, 0);
+        if (p.ev_off) ev_mark_realized(p, e);
       }
     };
     if (st0 != TL_OK) {
@@ -698,7 +714,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
       const tl_label L = make_label(c, LS, d0, p.rules);
       if (lane == 0) {
         p.labels[e] = L;
-        if (p.ev_off) ev_publish_agg(p, e, L.n_events);
+        if (p.ev_off) ev_mark_realized(p, e);
       }
     }
     __syncthreads();
@@ -706,7 +722,17 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     if (tid == 0 && e == gridDim.x) TL_STAMP(14);
     e = en;
   }
-  if (p.ev_off && warp == 0) ev_emit_all<DOFMAX>(p);
+  if (p.ev_off) ev_emit_all<DOFMAX>(p);
+  if (p.order) {  // the last CTA out leaves the length buckets at zero for the next launch
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(&p.tickets[2], 1u) == gridDim.x - 1) {
+        for (int b = 0; b < kLenBuckets; b++) p.tickets[kTkBucket + b] = 0u;
+        p.tickets[2] = 0u;
+      }
+    }
+  }
 }
 
 }  // namespace tl

@@ -412,6 +412,8 @@ size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
   const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
   return align256(n * kMtN * 4) + align256(n * sizeof(tl_script)) + align256(n * ms) +
          align256(n * ms * 4) + align256(n * 8)  // + event look-back states (tl_fuzz_ev)
+         + align256(n * 4)                        // + per-block realized counts
+         + align256(n * kLenBuckets * 4)          // + longest-first episode order
          + 256;                                   // + episode / emission tickets
 }
 
@@ -436,6 +438,10 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   char* base = reinterpret_cast<char*>(scratch);
   SynthParams sp;
   memset(&sp, 0, sizeof(sp));
+  // the claim counters come first: at a fixed offset for any n_env, so the
+  // zero state every call leaves them in holds across calls of other sizes
+  sp.tickets = reinterpret_cast<unsigned int*>(base);
+  base += 256;
   sp.states = reinterpret_cast<uint32_t*>(base);
   base += align256(n * kMtN * 4);
   sp.scripts = scripts ? scripts : reinterpret_cast<tl_script*>(base);
@@ -446,7 +452,10 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   base += align256(n * ms * 4);
   sp.ev_state = reinterpret_cast<unsigned long long*>(base);
   base += align256(n * 8);
-  sp.tickets = reinterpret_cast<unsigned int*>(base);
+  sp.ev_blk_done = reinterpret_cast<unsigned int*>(base);
+  base += align256(n * 4);
+  sp.order = reinterpret_cast<int32_t*>(base);
+  if (cap_per_env <= 64) sp.order = nullptr;  // every episode fits one wave: index order
   sp.seeds = seeds;
   sp.fuzz_subtask = subtask;
   sp.cfg = *cfg;

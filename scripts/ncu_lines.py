@@ -1,5 +1,5 @@
 """Per-CUDA-source-line totals (instructions executed, stall samples) from an
-ncu report: python scripts/ncu_lines.py rep.ncu-rep [top]"""
+ncu report: python scripts/ncu_lines.py rep.ncu-rep [top] [kernel-substring]"""
 import csv
 import io
 import subprocess
@@ -8,10 +8,12 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+only = sys.argv[3] if len(sys.argv) > 3 else None  # substring of the kernel name
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--print-source=cuda,sass", "--csv"],
                      capture_output=True, text=True).stdout
 agg = defaultdict(lambda: [0.0, 0.0, ""])
 fname = "?"
+func = ""
 head = None
 cur = None
 for row in csv.reader(io.StringIO(out)):
@@ -23,7 +25,10 @@ for row in csv.reader(io.StringIO(out)):
     if row[0] == "Line No":
         head = row
         continue
-    if head is None or row[0] == "Function Name":
+    if row[0] == "Function Name":
+        func = row[1]
+        continue
+    if head is None or (only and only not in func):
         continue
     d = dict(zip(head, row))
     if row[0].strip():
@@ -40,5 +45,7 @@ for row in csv.reader(io.StringIO(out)):
 tot_i = sum(v[0] for v in agg.values()) or 1
 tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total inst {tot_i:.0f}  samples {tot_s:.0f}")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+import os
+key = 0 if os.environ.get("SORT") == "inst" else 1
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
     print(f"{k[0]}:{k[1]:<5} inst {100*v[0]/tot_i:5.1f}%  stall {100*v[1]/tot_s:5.1f}%  {v[2]}")
