@@ -86,18 +86,27 @@ constexpr int kTkEmit = kTkBucket + kLenBuckets;  // event-list writing claims
 
 // ticket -> episode: tickets walk the length buckets from the longest down
 // (LPT order: a long episode claimed last would otherwise set the batch
-// time, synth.py run lengths vary ~4x around the mean)
-__device__ __forceinline__ int claim_episode(const SynthParams& p) {
+// time, synth.py run lengths vary ~4x around the mean).  The bucket sizes are
+// final once the reset kernel is done: one warp reads them once per launch
+// into shared memory (end[k] = exclusive end of buckets 15..15-k).
+__device__ __forceinline__ void load_bucket_ends(const SynthParams& p, int* end) {
+  const int lane = threadIdx.x & 31;
+  int c = lane < kLenBuckets ? (int)__ldcg(&p.tickets[kTkBucket + kLenBuckets - 1 - lane]) : 0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, c, d);
+    if (lane >= d) c += u;
+  }
+  if (lane < kLenBuckets) end[lane] = c;
+}
+
+__device__ __forceinline__ int claim_episode(const SynthParams& p, const int* end) {
   const int t = (int)atomicAdd(&p.tickets[0], 1u);
   if (p.order == nullptr || t >= p.n_env) return t;
-  int r = t;
-#pragma unroll 1
-  for (int b = kLenBuckets - 1; b >= 0; b--) {
-    const int c = (int)__ldcg(&p.tickets[kTkBucket + b]);
-    if (r < c) return __ldcg(&p.order[(int64_t)b * p.n_env + r]);
-    r -= c;
-  }
-  return p.n_env;  // unreachable: the buckets hold every episode
+  int k = 0;
+  while (k < kLenBuckets - 1 && t >= end[k]) k++;
+  const int start = k ? end[k - 1] : 0;
+  return __ldcg(&p.order[(int64_t)(kLenBuckets - 1 - k) * p.n_env + (t - start)]);
 }
 
 __device__ __forceinline__ bool in_alpha(int k, int ev) {

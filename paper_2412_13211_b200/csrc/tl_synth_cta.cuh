@@ -28,6 +28,23 @@
 
 namespace tl {
 
+#ifdef TL_PHASES
+// aggregate phase profiler (profiling build only, scripts/phase_totals.py):
+// thread 0 of every CTA adds the clock64 delta since its previous mark to
+// g_tl_phase[k]; g_tl_phase[15] counts waves
+__device__ unsigned long long g_tl_phase[16];
+#define TL_PH(k)                                                              \
+  do {                                                                        \
+    if (threadIdx.x == 0) {                                                   \
+      const long long _t = clock64();                                         \
+      atomicAdd(&g_tl_phase[(k)], (unsigned long long)(_t - ph_t));           \
+      ph_t = _t;                                                              \
+    }                                                                         \
+  } while (0)
+#else
+#define TL_PH(k) do { } while (0)
+#endif
+
 // W = records per wave = emission threads (warps 1..W/32); warp 0 runs the
 // cum chain.  W = 64 for long episodes; W = 32 (a 2-warp CTA, a quarter of
 // the ring, ~1.5x the CTAs per SM) when every episode fits one or two waves.
@@ -46,8 +63,9 @@ struct CtaCfg {
 template <int DOFMAX, int WAVE = kWave>
 struct CtaSmem {
   // script steps planned per window (scripts are re-planned window by
-  // window); the short-episode form plans 32 at a time to fit 12 CTAs/SM
-  static constexpr int kSteps = WAVE == 32 ? 32 : kMaxSteps;
+  // window); 48 keeps the 64-record form at 8 CTAs/SM (27.8 KB), the
+  // short-episode form plans 32 at a time to fit 12 CTAs/SM
+  static constexpr int kSteps = WAVE == 32 ? 32 : 48;
   uint32_t mt[2][kMtN];  // double-buffered MT state (current block, next block)
   uint32_t wb[CtaCfg<DOFMAX, WAVE>::kRing];
   int32_t gap[kSteps];
@@ -66,6 +84,7 @@ struct CtaSmem {
   int32_t misc[16];
   int32_t red[8];
   int32_t tk[2];            // claimed episode tickets (double-buffered by iteration)
+  int32_t bend[kLenBuckets];  // longest-first bucket ends (load_bucket_ends)
   tl_cset cs;
   // the CTA's next episode, copied in by cp.async while this one runs
   alignas(16) uint32_t mt_pf[kMtN];
@@ -269,7 +288,7 @@ __device__ void ev_emit_all(const SynthParams& p) {
 }
 
 template <bool FUZZ, int DOFMAX, int W>
-__global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
+__global__ void __launch_bounds__(W + 32, W == 64 ? 8 : 12)
     k_synth_cta(SynthParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CtaSmem<DOFMAX, W>& S = *reinterpret_cast<CtaSmem<DOFMAX, W>*>(smem_raw);
@@ -283,16 +302,22 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
   const uint2* ring2 = reinterpret_cast<const uint2*>(S.wb);
 
   int wave_no = 0;
-  bool pf = false;  // the next episode's inputs are in flight to S.*_pf
+  bool pf = false;
+#ifdef TL_PHASES
+  long long ph_t = clock64();
+#endif  // the next episode's inputs are in flight to S.*_pf
   // episodes by ticket, in claim order (dynamic load balance across CTAs);
   // the next episode is claimed at the top of the current one so its inputs
   // can be prefetched, parity-buffered in S.tk (>= 1 barrier per iteration)
-  if (tid == 0) S.tk[0] = claim_episode(p);
+  if (warp == 0 && p.order) load_bucket_ends(p, S.bend);
+  __syncwarp();
+  if (tid == 0) S.tk[0] = claim_episode(p, S.bend);
   __syncthreads();
   int e = S.tk[0];
   for (int it = 1; e < p.n_env; it++) {
-    if (tid == 0) S.tk[it & 1] = claim_episode(p);
+    if (tid == 0) S.tk[it & 1] = claim_episode(p, S.bend);
     if (tid == 0 && e == 0) TL_STAMP(10);
+    TL_PH(9);  // 9: end of the previous episode -> this one (claims, tail)
     // ---------------- script + seeded RNG state -------------------------------
     tl_script sc;
     int64_t rs;
@@ -367,6 +392,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
       continue;
     }
     if (tid == 0 && e == 0) TL_STAMP(11);
+    TL_PH(6);  // 6: episode prologue (state copy, init, prefetch issue)
     PlanSt ps;  // initial realizer state (synth.py:111-158)
     ps.force = (z.has_force && sc.initial_contact) ? 1.2 : 0.0;
     ps.grasped = sc.initial_grasped ? 1 : 0;
@@ -460,6 +486,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
       }
       __syncthreads();
       if (tid == 0 && e == 0) TL_STAMP(12);
+      TL_PH(7);  // 7: window plan (+ first block twist)
       const int perr = S.misc[0], pstep = S.misc[1];
       const int exc_rec = S.misc[14];
       const int r_begin = first_window ? 0 : tau_prev + 1;
@@ -503,12 +530,14 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
         seg_hint = S.misc[12];
         const int wbase = 20 + 8 * min(wave_no, 12);  // profiling build only
         if (tid == 0 && e == 0) TL_STAMP(wbase);
+        TL_PH(1);  // 1: record descriptors + block max
         while ((int)produced < need_max) {
           mt_twist_block_db<DOFMAX, W>(S.mt[mt_cur], S.mt[mt_cur ^ 1], S.wb, produced);
           mt_cur ^= 1;
           produced += kMtN;
         }
         if (tid == 0 && e == 0) TL_STAMP(wbase + 1);
+        TL_PH(2);  // 2: MT twists
         auto rnd = [&](int woff) {
           const uint2 wv = ring2[((uint32_t)woff & kMask) >> 1];
           return rand53(wv.x, wv.y);
@@ -522,6 +551,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
         if (tid == 0) S.misc[13] = 0x7fffffff;
         __syncthreads();
         if (tid == 0 && e == 0) TL_STAMP(wbase + 2);
+        TL_PH(3);  // 3: advance / apply draws
         double dist_rec = dist_carry;
         if (valid && z.has_goal) {
           const int ld = S.st[sidx].last_draw;
@@ -652,6 +682,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
           }
         }
         if (tid == 0 && e == 0) TL_STAMP(wbase + 3);
+        TL_PH(4);  // 4: cum chain || emission
         if (emitter) {
           uint32_t ind = 0, errb = 0, prev = ind_carry;
           if (valid) {
@@ -691,6 +722,10 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
         }
         // no barrier: S.part is rewritten only after the next wave's barriers
         if (tid == 0 && e == 0) TL_STAMP(wbase + 5);
+        TL_PH(5);  // 5: patch + fold
+#ifdef TL_PHASES
+        if (tid == 0) atomicAdd(&g_tl_phase[15], 1ull);
+#endif
         if (e == 0) wave_no++;
       }
       if (!err_code && perr) { err_code = perr; err_step = s_base + pstep; }
@@ -719,10 +754,13 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 7 : 12)
     }
     __syncthreads();
     if (tid == 0 && e == 0) TL_STAMP(13);
+    TL_PH(8);  // 8: label + window tail
     if (tid == 0 && e == gridDim.x) TL_STAMP(14);
     e = en;
   }
+  TL_PH(9);
   if (p.ev_off) ev_emit_all<DOFMAX>(p);
+  TL_PH(10);  // 10: event-list emission (incl. waiting for blocks)
   if (p.order) {  // the last CTA out leaves the length buckets at zero for the next launch
     __syncthreads();
     if (tid == 0) {

@@ -826,6 +826,17 @@ int tl_compact_records(const tl_records* src, int32_t n_env, const int64_t* dst_
   return check_launch();
 }
 
+#ifdef TL_PHASES
+extern "C" int tl_phase_read(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_tl_phase, sizeof(unsigned long long) * 16) != cudaSuccess) return TL_E_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_tl_phase, z, sizeof(z));
+  }
+  return TL_OK;
+}
+#endif
+
 #ifdef TL_PROFILE
 int tl_prof_read(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tl_prof, sizeof(unsigned long long) * 128) == cudaSuccess ? 0 : TL_E_CUDA;
