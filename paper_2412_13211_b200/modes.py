@@ -5,13 +5,16 @@ The 39 rule predicates are compiled into the device classifier
 reference's table shape {kind: {"success": [(mode_id, pred)], "failure":
 [...]}}; its predicates are handles on the device rules, so reordered or
 truncated tables (e.g. the --corrupt negative control, cli.py:232-238)
-run on the GPU too.
+run on the GPU too.  Tables may also hold arbitrary callables (the
+reference accepts any (mode_id, predicate) table, modes.py:235-253); those
+are called with the event view in table order, between device runs.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 from typing import Optional
 
+from . import _lib as L
 from .errors import UnknownMode, label_error
 from .events import EVENT_KINDS, EventKind, EventList
 from .model import SUBTASK_ORDER, SubtaskKind
@@ -96,48 +99,98 @@ class ModeLabel:
     success_at_end: bool
 
 
-def rules_to_ids(rules) -> Optional[list]:
-    """Reference-shaped rule table -> per (subtask, branch) device rule ids."""
-    if rules is None:
-        return None
-    out = []
-    for k in SUBTASK_ORDER:
-        table = rules.get(k) if hasattr(rules, "get") else None
-        if table is None:
-            out.append([[], []])
-            continue
-        branches = []
-        for b in ("success", "failure"):
-            ids = []
-            for mode_id, pred in table[b]:
-                if not isinstance(pred, DeviceRule):
-                    raise NotImplementedError(
-                        f"rule {mode_id!r}: only the builtin mode predicates run on the device")
-                ids.append(pred.index)
-            branches.append(ids)
-        out.append(branches)
+def _device_table(sub: int, ids) -> list:
+    """One rule run as a device table: the same ids on both branches of
+    subtask `sub` (the caller already chose the branch), nothing elsewhere."""
+    out = [[[], []] for _ in SUBTASK_ORDER]
+    out[sub] = [list(ids), list(ids)]
     return out
 
 
+class _EventView:
+    """What a rule predicate sees (the reference's _Ctx, modes.py:42-62):
+    kinds, size, d0, last(kind), has(kind).  Built once per classify call for
+    tables that hold host callables."""
+
+    __slots__ = ("kinds", "size", "d0", "_pos")
+
+    def __init__(self, events: EventList):
+        self.kinds = events.kinds()
+        self.size = len(self.kinds)
+        self.d0 = events.initial_dist_obj_goal
+        # later occurrences overwrite earlier ones: the value is the last index
+        self._pos = {k: i for i, k in enumerate(self.kinds)}
+
+    def last(self, kind: EventKind) -> int:
+        return self._pos.get(kind, -1)
+
+    def has(self, kind: EventKind) -> bool:
+        return kind in self._pos
+
+
+def _label(kind, mode_id, success_once):
+    return ModeLabel(subtask_kind=kind, mode_id=mode_id, is_success=success_once,
+                     success_once=success_once,
+                     success_at_end=mode_id in SUCCESS_AT_END_MODES[kind])
+
+
 def classify(events: EventList, rules: Optional[dict] = None) -> ModeLabel:
-    """One mode per event list (modes.py:235-253), on the GPU."""
+    """One mode per event list (modes.py:235-253): first match wins over the
+    success rules if Success occurs, else over the failure rules.
+
+    The builtin table (rules=None, or an empty table as `rules or MODE_RULES`
+    reads it) runs as one device classification.  A custom table is walked
+    in order: each maximal run of builtin predicates (DeviceRule) is one
+    device call over that run, returning the first match's position; any
+    other callable is the user's own Python and is called with the event
+    view, exactly when the reference would call it.  The returned mode_id is
+    the table entry's, not the predicate's own name."""
     from . import core
     kind = events.subtask_kind
-    if rules is not None:
-        rules[kind]  # KeyError for a table without this subtask, as the reference
-    ids = rules_to_ids(rules)
+    sub = SUBTASK_ORDER.index(kind)
     kinds = [EVENT_KINDS.index(e.kind) for e in events.events]
     d0 = events.initial_dist_obj_goal
-    lab = core.classify_lists([kinds], [SUBTASK_ORDER.index(kind)],
-                              [0.0 if d0 is None else float(d0)], [d0 is None], ids)[0]
-    st = int(lab["status"])
-    if st != 0:
-        raise label_error(st, kind.value, [e.kind.value for e in events.events],
-                          bool(lab["flags"] & 1))
-    m = MODE_LIST[int(lab["mode"])]
-    so = bool(lab["flags"] & 1)
-    return ModeLabel(subtask_kind=kind, mode_id=m, is_success=so, success_once=so,
-                     success_at_end=bool(lab["flags"] & 2))
+    d0_args = ([0.0 if d0 is None else float(d0)], [d0 is None])
+
+    def device(ids):
+        lab = core.classify_lists([kinds], [sub], *d0_args, ids)[0]
+        return int(lab["status"]), lab
+
+    if not rules:  # the builtin table, on the device
+        st, lab = device(None)
+        if st != 0:
+            raise label_error(st, kind.value, [e.kind.value for e in events.events],
+                              bool(lab["flags"] & 1))
+        so = bool(lab["flags"] & 1)
+        return ModeLabel(subtask_kind=kind, mode_id=MODE_LIST[int(lab["mode"])],
+                         is_success=so, success_once=so, success_at_end=bool(lab["flags"] & 2))
+    table = rules[kind]  # KeyError for a table without this subtask, as the reference
+    success_once = any(e.kind is EventKind.Success for e in events.events)
+    branch = list(table["success"] if success_once else table["failure"])
+    view = None
+    i = 0
+    while i < len(branch):
+        mode_id, pred = branch[i]
+        if isinstance(pred, DeviceRule):
+            j = i
+            while j < len(branch) and j - i < 16 and isinstance(branch[j][1], DeviceRule):
+                j += 1
+            ids = [p.index for _, p in branch[i:j]]
+            st, lab = device(_device_table(sub, ids))
+            if st == 0:  # the first run position holding the matched predicate
+                return _label(kind, branch[i + ids.index(int(lab["mode"]))][0], success_once)
+            if st != L.ERR_MODE_COVERAGE:
+                raise label_error(st, kind.value, [e.kind.value for e in events.events],
+                                  success_once)
+            i = j
+            continue
+        if view is None:
+            view = _EventView(events)
+        if pred(view):
+            return _label(kind, mode_id, success_once)
+        i += 1
+    raise label_error(L.ERR_MODE_COVERAGE, kind.value, [e.kind.value for e in events.events],
+                      success_once)
 
 
 @dataclass(frozen=True)

@@ -181,6 +181,34 @@ def test_mode_inventory_flags_and_coverage_error():
     assert T.last_index(_ev(T.SubtaskKind.Pick, [E.Contact, E.Grasped, E.Contact]), E.Contact) == 2
 
 
+def test_classify_custom_rule_tables_vs_reference():
+    """classify(events, rules) with arbitrary (mode_id, predicate) tables:
+    relabelled / reordered / repeated builtin predicates (device runs) mixed
+    with host callables, dropped catch-alls, empty and foreign tables --
+    against the reference's results (tests/golden/make_rules_golden.py)."""
+    import gzip
+    import os
+    import sys
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    from rule_recipes import build_table
+    with gzip.open(os.path.join(here, "rules.json.gz"), "rt") as f:
+        cases = json.load(f)
+    for c in cases:
+        kind = T.SubtaskKind(c["subtask"])
+        ev = _ev(kind, [E(k) for k in c["kinds"]], c["d0"])
+        table = build_table(c["recipe"], T.MODE_RULES, T.SubtaskKind, T.EventKind)
+        if "error" in c:
+            with pytest.raises(Exception) as ei:
+                T.classify(ev, rules=table)
+            assert type(ei.value).__name__ == c["error"][0], c
+            if c["error"][0] != "KeyError":
+                assert str(ei.value) == c["error"][1], c
+        else:
+            lab = T.classify(ev, rules=table)
+            assert [lab.mode_id, lab.success_once, lab.success_at_end] == c["result"], c
+
+
 # -- synth (reference test_synth.py) ---------------------------------------------
 
 def test_realize_is_deterministic_and_valid():
