@@ -255,7 +255,10 @@ struct MtLane {
   }
   __device__ __forceinline__ uint32_t genrand() {
     if (idx < pre) return mt_temper(mt[idx++]);
-    pre = 0;  // first block prefix consumed; continue lazily
+    if (pre) {  // first block prefix consumed; continue lazily
+      pre = 0;
+      if (idx == kMtN) idx = 0;  // the whole first block was prepared
+    }
     const int i = idx;
     const int i1 = i + 1 == kMtN ? 0 : i + 1;
     const int src = i < kMtN - kMtM ? i + kMtM : i - (kMtN - kMtM);
@@ -263,6 +266,52 @@ struct MtLane {
     mt[i] = v;
     idx = i1;
     return mt_temper(v);
+  }
+  // the same for the whole first block (words [0, 624)), by the 32 lanes of
+  // a warp in CPython's three dependency phases (0..226 read old words only,
+  // 227..453 read new words 0..226, 454..623 read new 227..396 and word 0);
+  // every lane of the warp calls it, then one lane samples with pre = 624
+  __device__ __forceinline__ void prepare_block_warp() {
+    const int lane = lane_id();
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int i = lane + 32 * k;
+      if (i < kMtN - kMtM) v[k] = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int i = lane + 32 * k;
+      if (i < kMtN - kMtM) mt[i] = v[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int i = kMtN - kMtM + lane + 32 * k;
+      if (i < 2 * (kMtN - kMtM)) v[k] = mt_mix(mt[i], mt[i + 1], mt[i - (kMtN - kMtM)]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int i = kMtN - kMtM + lane + 32 * k;
+      if (i < 2 * (kMtN - kMtM)) mt[i] = v[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      const int i = 2 * (kMtN - kMtM) + lane + 32 * k;
+      if (i < kMtN) v[k] = mt_mix(mt[i], mt[i + 1 == kMtN ? 0 : i + 1], mt[i - (kMtN - kMtM)]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      const int i = 2 * (kMtN - kMtM) + lane + 32 * k;
+      if (i < kMtN) mt[i] = v[k];
+    }
+    __syncwarp();
+    idx = 0;
+    pre = kMtN;
   }
   __device__ __forceinline__ double random() {
     uint32_t a = genrand() >> 5, b = genrand() >> 6;

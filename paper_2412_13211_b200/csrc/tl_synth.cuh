@@ -60,19 +60,14 @@ struct SynthParams {
   tl_records out;
   uint8_t* step_mask;
   tl_label* labels;
-  // optional fused event lists (k_synth_cta): ordered (kind, t) at ev_off[e]
-  int64_t* ev_off;
-  uint8_t* ev_kind;
-  int32_t* ev_t;
-  unsigned long long* ev_state;  // [n_env/32] block look-back status, zeroed per launch
-  unsigned int* ev_blk_done;     // [n_env/32] realized episodes per block, zeroed per launch
-  // claim counters: [0] episodes, [1] event-list offset blocks,
-  // [kTkEmit] event-list writing (zeroed by the reset kernel),
-  // [2] exited CTAs, [4 + b] episodes in length bucket b (left
-  // at zero by every k_synth_cta launch; zero-filled scratch before the first).
-  // k_synth_cta takes episodes by ticket, so every cross-CTA wait targets an
-  // episode already claimed by a running CTA (no co-residency assumption,
-  // see ev_emit_all)
+  // tl_fuzz_ev: k_scan_emit's tile states + tile counter ([ev_zero] entries),
+  // zeroed by the reset kernel (no memset node in the step graph)
+  unsigned long long* ev_state;
+  int32_t ev_zero;
+  // claim counters: [0] episodes (zeroed by the reset kernel), [2] exited
+  // CTAs, [4 + b] episodes in length bucket b (left at zero by every
+  // k_synth_cta launch; zero-filled scratch before the first).  k_synth_cta
+  // takes episodes by ticket and never waits on another CTA.
   unsigned int* tickets;
   // longest-first episode order (fuzz, long-episode configs): bucket b holds
   // the episodes of b+1 64-record waves (b = 15: 16 or more) at
@@ -82,7 +77,6 @@ struct SynthParams {
 
 constexpr int kLenBuckets = 16;
 constexpr int kTkBucket = 4;  // tickets[kTkBucket + b]
-constexpr int kTkEmit = kTkBucket + kLenBuckets;  // event-list writing claims
 
 // ticket -> episode: tickets walk the length buckets from the longest down
 // (LPT order: a long episode claimed last would otherwise set the batch
@@ -400,6 +394,42 @@ __device__ __forceinline__ StepSt make_st(const RzConst& z, const PlanSt& p, int
   return s;
 }
 
+// random_script + the episode's script record, length bucket and record
+// layout (one thread; R = the freshly seeded script RNG)
+__device__ __forceinline__ void reset_script(const SynthParams& p, int64_t e, int64_t seed,
+                                             MtLane& R) {
+  const int ms = p.cfg.max_events + 4;
+  tl_script t;
+  uint8_t* sk = p.step_kind + e * ms;
+  int32_t* sg = p.step_gap + e * ms;
+  // at most max_events + 4 = ms steps are ever produced (synth.py:463-505)
+  const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t, ms);
+  int64_t nr = 1;
+  for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += sg[i];
+  const int64_t tmin = ns > 0 ? 0 : 1;
+  nr += t.tail > tmin ? t.tail : tmin;
+  if (nr < 2) nr = 2;
+  t.step_off = e * ms;
+  t.seed = seed ^ 0x5EED;
+  t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
+  p.scripts[e] = t;
+  if (p.order) {  // length bucket for the realize kernel's longest-first claims
+    const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / 64);
+    const unsigned slot = atomicAdd(&p.tickets[kTkBucket + b], 1u);
+    p.order[(int64_t)b * p.n_env + slot] = (int32_t)e;
+  }
+  if (e < p.ev_zero) p.ev_state[e] = 0ull;  // k_scan_emit tile state of this launch
+  if (p.out.rec_start) {  // record layout (tl_fuzz); the env reset has none
+    p.out.rec_start[e] = e * p.cap_per_env;
+    p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;
+  }
+}
+
+__device__ __forceinline__ void reset_counters(const SynthParams& p) {
+  p.tickets[0] = 0u;  // episode claims
+  for (int i = p.n_env; i < p.ev_zero; i++) p.ev_state[i] = 0ull;  // tiny batches
+}
+
 // ---- reset: seeding + random_script, one thread per RNG ---------------------
 // CPython seeding is a 1247-step serial chain per state, so it runs one
 // state per thread (32 chains per warp) into padded shared-memory rows
@@ -423,13 +453,8 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
   const bool valid = (lane >> 1) < EPW && e < p.n_env;
   uint32_t* row = STREAM ? rows + (lane < 2 * EPW ? lane >> 1 : 0) * kRowWords
                          : rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
-  const int ms = p.cfg.max_events + 4;
   if (lane == 0) TL_STAMP(0);
-  if (blockIdx.x == 0 && lane == 0 && p.tickets) {
-    p.tickets[0] = 0u;  // episode claims
-    p.tickets[1] = 0u;  // event-list block claims
-    p.tickets[kTkEmit] = 0u;
-  }
+  if (blockIdx.x == 0 && lane == 0 && p.tickets) reset_counters(p);
   if (valid) {
     const int64_t seed = p.seeds[e];
     // odd lanes: realize RNG, final state written straight to global memory
@@ -443,36 +468,41 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
     if (!(lane & 1)) {
       MtLane R{row, 0, 0};
       R.prepare(128);
-      tl_script t;
-      uint8_t* sk = p.step_kind + e * ms;
-      int32_t* sg = p.step_gap + e * ms;
-      // at most max_events + 4 = ms steps are ever produced (synth.py:463-505)
-      const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t, ms);
-      int64_t nr = 1;
-      for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += sg[i];
-      const int64_t tmin = ns > 0 ? 0 : 1;
-      nr += t.tail > tmin ? t.tail : tmin;
-      if (nr < 2) nr = 2;
-      t.step_off = e * ms;
-      t.seed = seed ^ 0x5EED;
-      t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
-      p.scripts[e] = t;
-      if (p.order) {  // length bucket for the realize kernel's longest-first claims
-        const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / 64);
-        const unsigned slot = atomicAdd(&p.tickets[kTkBucket + b], 1u);
-        p.order[(int64_t)b * p.n_env + slot] = (int32_t)e;
-      }
-      if (p.ev_off && (e << 5) < p.n_env) {  // event-list block state of this launch
-        p.ev_state[e] = 0ull;
-        p.ev_blk_done[e] = 0u;
-      }
-      if (p.out.rec_start) {  // record layout (tl_fuzz); the env reset has none
-        p.out.rec_start[e] = e * p.cap_per_env;
-        p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;
-      }
+      reset_script(p, e, seed, R);
     }
   }
   if (lane == 0) TL_STAMP(2);
+}
+
+// Latency form (batches up to a few episodes per SM): a CTA of E warps owns E
+// episodes.  Warp 0 seeds all 2E states (lane 2j: script RNG of episode j into
+// shared row j, lane 2j+1: realize RNG straight to global memory), so the
+// 1247-step chains cost one warp of issue per CTA; then warp j regenerates
+// episode j's first MT block with all 32 lanes and its lane 0 samples
+// random_script from it -- one sampler per warp, no divergence between
+// episodes' branchy sampling code.
+template <int E>
+__global__ void __launch_bounds__(E * 32) k_fuzz_reset_w(SynthParams p) {
+  static_assert(E >= 1 && E <= 16, "2E seeding lanes in one warp");
+  extern __shared__ uint32_t rows[];  // [E][kRowWords]
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.tickets) reset_counters(p);
+  if (warp == 0) {
+    const int j = lane >> 1;
+    const int64_t e = e0 + j;
+    if (j < E && e < p.n_env) {
+      const int64_t seed = p.seeds[e];
+      mt_seed_lane_stream((lane & 1) ? (seed ^ 0x5EED) : seed,
+                          (lane & 1) ? p.states + e * kMtN : rows + j * kRowWords);
+    }
+  }
+  __syncthreads();
+  const int64_t e = e0 + warp;
+  if (e >= p.n_env) return;
+  MtLane R{rows + warp * kRowWords, 0, 0};
+  R.prepare_block_warp();
+  if (lane == 0) reset_script(p, e, p.seeds[e], R);
 }
 
 // realize path: seed the realize RNG of given scripts (one thread per state,
@@ -480,7 +510,7 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
 __global__ void __launch_bounds__(128) k_seed_states(SynthParams p) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e == 0 && p.tickets) {
-    p.tickets[0] = 0u; p.tickets[1] = 0u; p.tickets[kTkEmit] = 0u;
+    p.tickets[0] = 0u;
   }
   if (e < p.n_env) mt_seed_lane_stream(p.scripts[e].seed, p.states + e * kMtN);
 }

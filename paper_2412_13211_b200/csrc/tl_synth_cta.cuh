@@ -21,8 +21,10 @@
 //   * each emission warp folds its 32 event masks into a partial label
 //     state, combined in order by warp 0; persistent CTAs prefetch their
 //     next episode's seeded state and script by cp.async;
-//   * tl_fuzz_ev: the ordered event lists are written by the same kernel
-//     after a warp-wide decoupled look-back over the episodes' event counts.
+//   * tl_fuzz_ev: the ordered event lists are written by k_scan_emit right
+//     after this kernel (tl_label.cuh): an in-kernel form had to wait for the
+//     last realized episode of every 32-episode block, and with longest-first
+//     claims that is the end of the batch for nearly every block.
 #pragma once
 #include "tl_synth.cuh"
 
@@ -174,119 +176,6 @@ __device__ __forceinline__ int block_max(int v, int32_t* red) {
   return m;  // red is rewritten only after later barriers of the wave
 }
 
-// ---- fused event lists ---------------------------------------------------------
-// events.py:109-191 without a separate scan kernel.  A CTA that finishes an
-// episode (label written) counts it in its 32-episode block's counter
-// (release: fence, then the atomic).  Once a CTA's episode claims are
-// exhausted, its warps take blocks by a second ticket, each once the block's
-// 32 episodes are realized (one acquire load per back-off interval, no
-// per-episode spinning while other CTAs on the SM still realize): warp scan
-// of the 32 labels' n_events, a decoupled look-back over the preceding
-// blocks' statuses (aggregate or inclusive prefix, ev_state[block]), ev_off;
-// then the ordered (kind, t) lists from the step masks, an episode per claim.
-// Progress: the wait targets episodes that were all claimed by CTAs that
-// were running when they claimed them, and realizing an episode waits on
-// nothing -- no assumption that the whole grid is co-resident (concurrent
-// kernels, MPS or green-context SM limits cannot hang it).
-__device__ __forceinline__ void ev_mark_realized(const SynthParams& p, int e) {
-  __threadfence();  // the episode's label, step masks and n_rec before the count
-  atomicAdd(&p.ev_blk_done[e >> 5], 1u);
-}
-
-__device__ __forceinline__ int64_t ev_lookback(const SynthParams& p, int blk) {
-  const int lane = lane_id();
-  volatile unsigned long long* st = p.ev_state;
-  int64_t prefix = 0;
-  int j = blk - 1;
-  while (j >= 0) {
-    const int idx = j - lane;
-    const unsigned long long v = idx >= 0 ? st[idx] : kTilePrefix;
-    const unsigned long long flag = v & ~kTileValMask;
-    const unsigned pm = __ballot_sync(kFull, flag == kTilePrefix);
-    const unsigned zm = __ballot_sync(kFull, flag == 0);
-    const int lim = pm ? __ffs(pm) - 1 : 31;             // lanes 0..lim are needed
-    const unsigned need = lim == 31 ? kFull : ((2u << lim) - 1u);
-    if (zm & need) {                                      // a predecessor block not published yet
-      __nanosleep(32);
-      continue;
-    }
-    int64_t c = lane <= lim ? (int64_t)(v & kTileValMask) : 0;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
-    prefix += c;
-    if (pm) break;
-    j -= 32;
-  }
-  return prefix;
-}
-
-// every warp of every CTA, after its episode loop (all episodes claimed):
-// phase A resolves ev_off by 32-episode blocks (each once its episodes are
-// realized), phase B writes one episode's list per warp claim (all warps of
-// the finished CTAs share the writing)
-template <int DOFMAX>
-__device__ void ev_emit_all(const SynthParams& p) {
-  const int lane = lane_id();
-  const int n_blk = (p.n_env + 31) / 32;
-  for (;;) {  // phase A: offsets, a block as soon as its 32 episodes are realized
-    int blk = 0;
-    if (lane == 0) {
-      blk = (int)atomicAdd(&p.tickets[1], 1u);
-      const unsigned want = (unsigned)min(32, p.n_env - blk * 32);
-      for (unsigned ns = 64; blk < n_blk && ld_acquire_u32(&p.ev_blk_done[blk]) < want;
-           ns = min(ns * 2, 256u))
-        __nanosleep(ns);
-    }
-    blk = __shfl_sync(kFull, blk, 0);
-    if (blk >= n_blk) break;
-    __threadfence();
-    const int e = blk * 32 + lane;
-    const int n_ev = e < p.n_env ? __ldcg(&p.labels[e].n_events) : 0;  // 0 for failed episodes
-    const int incl = warp_incl_scan(n_ev);
-    const int total = __shfl_sync(kFull, incl, 31);
-    if (lane == 0) atomicExch(&p.ev_state[blk], kTileAgg | (unsigned long long)total);
-    const int64_t prefix = ev_lookback(p, blk);
-    const int64_t my_off = prefix + incl - n_ev;
-    if (e < p.n_env) p.ev_off[e] = my_off;
-    if (e == p.n_env - 1) p.ev_off[p.n_env] = my_off + n_ev;
-    __threadfence();  // the block's ev_off before its inclusive-prefix status
-    __syncwarp();
-    if (lane == 0) atomicExch(&p.ev_state[blk], kTilePrefix | (unsigned long long)(prefix + total));
-  }
-  const int sub = p.fuzz_subtask;  // fused event lists are a fuzz (single-subtask) path
-  volatile unsigned long long* st = p.ev_state;
-  for (;;) {  // phase B: lists
-    int e = 0;
-    if (lane == 0) e = (int)atomicAdd(&p.tickets[kTkEmit], 1u);
-    e = __shfl_sync(kFull, e, 0);
-    if (e >= p.n_env) break;
-    // the block's inclusive prefix is published after its episodes were realized
-    // and its ev_off written: only then are the label and the offsets final
-    while ((st[e >> 5] & ~kTileValMask) != kTilePrefix) __nanosleep(64);
-    __threadfence();
-    if (__ldcg(&p.labels[e].n_events) == 0) continue;
-    int64_t base = __ldcg(&p.ev_off[e]);
-    const int64_t rs = __ldcg(&p.out.rec_start[e]);
-    const int n = __ldcg(&p.out.n_rec[e]);
-    for (int t0 = 0; t0 < n; t0 += 32) {
-      const int t = t0 + lane;
-      const uint32_t mask = t < n ? __ldcg(&p.step_mask[rs + t]) : 0u;
-      const int cnt = __popc(mask);
-      const int inc = warp_incl_scan(cnt);
-      int64_t pos = base + inc - cnt;
-      uint32_t m = mask;
-      while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
-        p.ev_kind[pos] = kAlpha[sub][k];
-        p.ev_t[pos] = t;
-        pos++;
-      }
-      base += __shfl_sync(kFull, inc, 31);
-    }
-  }
-}
-
 template <bool FUZZ, int DOFMAX, int W>
 __global__ void __launch_bounds__(W + 32, W == 64 ? 8 : 12)
     k_synth_cta(SynthParams p) {
@@ -345,7 +234,6 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 8 : 12)
         L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;
-        if (p.ev_off) ev_mark_realized(p, e);
       }
       __syncthreads();
       e = S.tk[it & 1];
@@ -382,7 +270,6 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 8 : 12)
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;
         if (FUZZ) p.out.n_rec[e] = 0;
-        if (p.ev_off) ev_mark_realized(p, e);
       }
     };
     if (st0 != TL_OK) {
@@ -747,10 +634,7 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 8 : 12)
       fail(err_code, err_step);
     } else if (warp == 0) {
       const tl_label L = make_label(c, LS, d0, p.rules);
-      if (lane == 0) {
-        p.labels[e] = L;
-        if (p.ev_off) ev_mark_realized(p, e);
-      }
+      if (lane == 0) p.labels[e] = L;
     }
     __syncthreads();
     if (tid == 0 && e == 0) TL_STAMP(13);
@@ -759,8 +643,6 @@ __global__ void __launch_bounds__(W + 32, W == 64 ? 8 : 12)
     e = en;
   }
   TL_PH(9);
-  if (p.ev_off) ev_emit_all<DOFMAX>(p);
-  TL_PH(10);  // 10: event-list emission (incl. waiting for blocks)
   if (p.order) {  // the last CTA out leaves the length buckets at zero for the next launch
     __syncthreads();
     if (tid == 0) {

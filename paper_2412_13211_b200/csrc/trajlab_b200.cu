@@ -320,6 +320,17 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
 // episodes (measured: scripts/reset_epw_ab.sh, scripts/reset_epw_ab2.sh)
 static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   const int n = sp.n_env, sms = sm_count();
+  // up to 64 episodes per SM: the warp-per-sampler latency form
+  const char* fw = ab_env("TL_RESET_W");
+  const int wform = fw ? atoi(fw) : ((int64_t)n <= (int64_t)sms * 64 ? 8 : 0);
+  if (wform == 8) {
+    k_fuzz_reset_w<8><<<(n + 7) / 8, 8 * 32, 8 * kRowWords * 4, S(stream)>>>(sp);
+    return;
+  }
+  if (wform == 16) {
+    k_fuzz_reset_w<16><<<(n + 15) / 16, 16 * 32, 16 * kRowWords * 4, S(stream)>>>(sp);
+    return;
+  }
   const char* force = ab_env("TL_RESET_EPW");
   const int epw = force ? atoi(force)
                         : (int64_t)n <= (int64_t)sms * 8 ? 1 : (int64_t)n <= (int64_t)sms * 64 ? 4 : 8;
@@ -411,8 +422,7 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t tl_fuzz_scratch_bytes(int32_t n_env, const tl_fuzz_cfg* cfg) {
   const size_t n = n_env > 0 ? (size_t)n_env : 1, ms = cfg ? (size_t)(cfg->max_events + 4) : 64;
   return align256(n * kMtN * 4) + align256(n * sizeof(tl_script)) + align256(n * ms) +
-         align256(n * ms * 4) + align256(n * 8)  // + event look-back states (tl_fuzz_ev)
-         + align256(n * 4)                        // + per-block realized counts
+         align256(n * ms * 4) + align256((n + 1) * 8)  // + k_scan_emit tile states (tl_fuzz_ev)
          + align256(n * kLenBuckets * 4)          // + longest-first episode order
          + 256;                                   // + episode / emission tickets
 }
@@ -451,9 +461,7 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   sp.step_gap = script_gap ? script_gap : reinterpret_cast<int32_t*>(base);
   base += align256(n * ms * 4);
   sp.ev_state = reinterpret_cast<unsigned long long*>(base);
-  base += align256(n * 8);
-  sp.ev_blk_done = reinterpret_cast<unsigned int*>(base);
-  base += align256(n * 4);
+  base += align256((n + 1) * 8);
   sp.order = reinterpret_cast<int32_t*>(base);
   if (cap_per_env <= 64) sp.order = nullptr;  // every episode fits one wave: index order
   sp.seeds = seeds;
@@ -467,10 +475,14 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   sp.out = *out;
   sp.step_mask = step_mask;
   sp.labels = labels;
-  if (ev_off) {  // tl_fuzz_ev: fused ordered event lists
-    sp.ev_off = ev_off;
-    sp.ev_kind = ev_kind;
-    sp.ev_t = ev_t;  // ev_state is zeroed by the reset kernel (no memset node)
+  if (ev_off) {  // tl_fuzz_ev: ordered event lists by k_scan_emit right after the realize kernel
+    const int tiles = (n_env + 31) / 32;
+    sp.ev_zero = tiles + 1;  // tile states + the tile counter, zeroed by the reset kernel
+    const int rc = launch_synth(sp, true, stream);
+    if (rc != TL_OK) return rc;
+    k_scan_emit<<<tiles, 1024, 0, S(stream)>>>(step_mask, out->rec_start, out->n_rec, labels, n_env,
+                                                ev_off, ev_kind, ev_t, sp.ev_state);
+    return check_launch();
   }
   return launch_synth(sp, true, stream);
 }
