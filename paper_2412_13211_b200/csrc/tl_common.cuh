@@ -241,6 +241,7 @@ struct MtLane {
   uint32_t* mt;
   int idx;  // next word of the current block (0 right after seeding)
   int pre;  // words [0, pre) of the first block are already regenerated in place
+  const uint32_t* tw = nullptr;  // their tempered values (prepare_block_warp), or null
   // regenerate words [0, n) (n <= 227: they read old words only) with
   // independent loads, so the serial sampler only tempers them
   __device__ __forceinline__ void prepare(int n) {
@@ -254,7 +255,11 @@ struct MtLane {
     pre = n;
   }
   __device__ __forceinline__ uint32_t genrand() {
-    if (idx < pre) return mt_temper(mt[idx++]);
+    if (idx < pre) {
+      const uint32_t x = tw ? tw[idx] : mt_temper(mt[idx]);
+      idx++;
+      return x;
+    }
     if (pre) {  // first block prefix consumed; continue lazily
       pre = 0;
       if (idx == kMtN) idx = 0;  // the whole first block was prepared
@@ -270,8 +275,9 @@ struct MtLane {
   // the same for the whole first block (words [0, 624)), by the 32 lanes of
   // a warp in CPython's three dependency phases (0..226 read old words only,
   // 227..453 read new words 0..226, 454..623 read new 227..396 and word 0);
-  // every lane of the warp calls it, then one lane samples with pre = 624
-  __device__ __forceinline__ void prepare_block_warp() {
+  // every lane of the warp calls it, then one lane samples with pre = 624;
+  // `tout` receives the tempered words (the serial sampler only loads them)
+  __device__ __forceinline__ void prepare_block_warp(uint32_t* tout) {
     const int lane = lane_id();
     uint32_t v[8];
 #pragma unroll
@@ -283,7 +289,7 @@ struct MtLane {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const int i = lane + 32 * k;
-      if (i < kMtN - kMtM) mt[i] = v[k];
+      if (i < kMtN - kMtM) { mt[i] = v[k]; tout[i] = mt_temper(v[k]); }
     }
     __syncwarp();
 #pragma unroll
@@ -295,7 +301,7 @@ struct MtLane {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const int i = kMtN - kMtM + lane + 32 * k;
-      if (i < 2 * (kMtN - kMtM)) mt[i] = v[k];
+      if (i < 2 * (kMtN - kMtM)) { mt[i] = v[k]; tout[i] = mt_temper(v[k]); }
     }
     __syncwarp();
 #pragma unroll
@@ -307,11 +313,12 @@ struct MtLane {
 #pragma unroll
     for (int k = 0; k < 6; k++) {
       const int i = 2 * (kMtN - kMtM) + lane + 32 * k;
-      if (i < kMtN) mt[i] = v[k];
+      if (i < kMtN) { mt[i] = v[k]; tout[i] = mt_temper(v[k]); }
     }
     __syncwarp();
     idx = 0;
     pre = kMtN;
+    tw = tout;
   }
   __device__ __forceinline__ double random() {
     uint32_t a = genrand() >> 5, b = genrand() >> 6;

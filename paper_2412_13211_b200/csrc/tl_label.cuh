@@ -1312,22 +1312,30 @@ __global__ void __launch_bounds__(1024)
     }
     const int64_t total = __shfl_sync(kFull, incl, 31);
     int64_t prefix = 0;
-    if (lane == 0) {
+    if (tile == 0) {
+      if (lane == 0) atomicExch(tile_state, kTilePrefix | (unsigned long long)total);
+    } else {
+      if (lane == 0) atomicExch(tile_state + tile, kTileAgg | (unsigned long long)total);
+      // warp-wide decoupled look-back: 32 predecessor tiles per probe, summed
+      // up to the nearest one that already holds its inclusive prefix
       volatile unsigned long long* st = tile_state;
-      if (tile == 0) {
-        atomicExch(tile_state, kTilePrefix | (unsigned long long)total);
-      } else {
-        atomicExch(tile_state + tile, kTileAgg | (unsigned long long)total);
-        for (int t = tile - 1; t >= 0;) {
-          const unsigned long long v = st[t];
-          const unsigned long long flag = v & ~kTileValMask;
-          if (!flag) continue;  // predecessor not published yet
-          prefix += (int64_t)(v & kTileValMask);
-          if (flag == kTilePrefix) break;
-          t--;
-        }
-        atomicExch(tile_state + tile, kTilePrefix | (unsigned long long)(prefix + total));
+      for (int j = tile - 1; j >= 0;) {
+        const int idx = j - lane;
+        const unsigned long long v = idx >= 0 ? st[idx] : kTilePrefix;
+        const unsigned long long flag = v & ~kTileValMask;
+        const unsigned pm = __ballot_sync(kFull, flag == kTilePrefix);
+        const unsigned zm = __ballot_sync(kFull, flag == 0);
+        const int lim = pm ? __ffs(pm) - 1 : 31;  // lanes 0..lim are needed
+        const unsigned need = lim == 31 ? kFull : ((2u << lim) - 1u);
+        if (zm & need) continue;                  // a predecessor not published yet
+        int64_t c = lane <= lim ? (int64_t)(v & kTileValMask) : 0;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+        prefix += c;
+        if (pm) break;
+        j -= 32;
       }
+      if (lane == 0) atomicExch(tile_state + tile, kTilePrefix | (unsigned long long)(prefix + total));
     }
     prefix = __shfl_sync(kFull, prefix, 0);
     const int64_t off = prefix + incl - cnt;
@@ -1342,21 +1350,47 @@ __global__ void __launch_bounds__(1024)
   const int64_t rs = rec_start[e];
   const int n = n_rec[e];
   int64_t base = s_off[warp];
-  for (int t0 = 0; t0 < n; t0 += 32) {
-    const int t = t0 + lane;
-    const uint32_t mask = t < n ? step_mask[rs + t] : 0u;
-    const int cnt = __popc(mask);
-    const int incl = warp_incl_scan(cnt);
-    int64_t pos = base + incl - cnt;
-    uint32_t m = mask;
-    while (m) {
-      const int k = __ffs(m) - 1;
-      m &= m - 1;
-      ev_kind[pos] = kAlpha[sub][k];
-      ev_t[pos] = t;
-      pos++;
+  // four records per lane (one 32-bit load when the episode's masks are
+  // 4-byte aligned), up to eight 128-record chunks loaded before any is
+  // processed: the longest episode's chain of dependent loads sets the time
+  const uint8_t* sm = step_mask + rs;
+  const bool al = (reinterpret_cast<uintptr_t>(sm) & 3) == 0;
+  for (int c0 = 0; c0 < n; c0 += 1024) {
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int t = c0 + 128 * k + 4 * lane;
+      uint32_t v = 0u;
+      if (al && t + 3 < n) {
+        v = *reinterpret_cast<const uint32_t*>(sm + t);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; b++)
+          if (t + b < n) v |= (uint32_t)sm[t + b] << (8 * b);
+      }
+      w[k] = v;
     }
-    base += __shfl_sync(kFull, incl, 31);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (c0 + 128 * k >= n) break;  // warp-uniform
+      const int t4 = c0 + 128 * k + 4 * lane;
+      const uint32_t v = w[k];
+      const int cnt = __popc(v);
+      const int incl = warp_incl_scan(cnt);
+      int64_t pos = base + incl - cnt;
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        uint32_t m = (v >> (8 * b)) & 0xffu;
+        while (m) {
+          const int q = __ffs(m) - 1;
+          m &= m - 1;
+          ev_kind[pos] = kAlpha[sub][q];
+          ev_t[pos] = t4 + b;
+          pos++;
+        }
+      }
+      base += __shfl_sync(kFull, incl, 31);
+    }
   }
 }
 

@@ -131,12 +131,13 @@ __device__ int choices_idx(MtLane& R, const double* w, int n) {
 // random_script (synth.py:363-507), one thread.  Returns n_steps, or -1
 // when the script does not fit `cap` steps (never for cap = max_events + 4).
 __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
-                             uint8_t* sk, int32_t* sg, tl_script& sc, int cap) {
+                             uint8_t* sk, int32_t* sg, tl_script& sc, int cap, int64_t& gaps) {
   int n = 0;
   bool overflow = false;
+  gaps = 0;  // sum of the stored steps' gaps
   auto push = [&](int ev) {
     const int32_t g = R.randint(1, cfg.max_gap);
-    if (n < cap) { sk[n] = (uint8_t)ev; sg[n] = g; n++; } else overflow = true;
+    if (n < cap) { sk[n] = (uint8_t)ev; sg[n] = g; gaps += g; n++; } else overflow = true;
   };
   sc.tail = R.randint(1, cfg.max_tail);                                  // :372
   sc.initial_grasped = 0;
@@ -227,7 +228,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
       for (int i = 0; i < 4; i++) g[i] = R.randint(1, cfg.max_gap);
       const int brk = kind == TL_PICK ? TL_EV_DROPPED : kind == TL_PLACE ? TL_EV_OBJ_LEFT_GOAL
                     : kind == TL_OPEN ? TL_EV_CLOSED : TL_EV_OPEN;
-      if (n < cap) { sk[n] = (uint8_t)brk; sg[n] = g[kind]; n++; } else overflow = true;
+      if (n < cap) { sk[n] = (uint8_t)brk; sg[n] = g[kind]; gaps += g[kind]; n++; } else overflow = true;
     } else if (suffix == 2) {
       push(TL_EV_EXCESSIVE_COLLISIONS);
     } else if (suffix == 3) {
@@ -403,9 +404,9 @@ __device__ __forceinline__ void reset_script(const SynthParams& p, int64_t e, in
   uint8_t* sk = p.step_kind + e * ms;
   int32_t* sg = p.step_gap + e * ms;
   // at most max_events + 4 = ms steps are ever produced (synth.py:463-505)
-  const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t, ms);
-  int64_t nr = 1;
-  for (int i = 0; i < (ns < 0 ? 0 : ns); i++) nr += sg[i];
+  int64_t gaps;
+  const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t, ms, gaps);
+  int64_t nr = 1 + (ns < 0 ? 0 : gaps);
   const int64_t tmin = ns > 0 ? 0 : 1;
   nr += t.tail > tmin ? t.tail : tmin;
   if (nr < 2) nr = 2;
@@ -474,6 +475,7 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
   if (lane == 0) TL_STAMP(2);
 }
 
+#ifdef TL_AB
 // Latency form (batches up to a few episodes per SM): a CTA of E warps owns E
 // episodes.  Warp 0 seeds all 2E states (lane 2j: script RNG of episode j into
 // shared row j, lane 2j+1: realize RNG straight to global memory), so the
@@ -484,10 +486,11 @@ __global__ void __launch_bounds__(32) k_fuzz_reset(SynthParams p) {
 template <int E>
 __global__ void __launch_bounds__(E * 32) k_fuzz_reset_w(SynthParams p) {
   static_assert(E >= 1 && E <= 16, "2E seeding lanes in one warp");
-  extern __shared__ uint32_t rows[];  // [E][kRowWords]
+  extern __shared__ uint32_t rows[];  // [E][kRowWords] states, then [E][kMtN] tempered words
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t e0 = (int64_t)blockIdx.x * E;
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.tickets) reset_counters(p);
+  if (threadIdx.x == 0) TL_STAMP(0);
   if (warp == 0) {
     const int j = lane >> 1;
     const int64_t e = e0 + j;
@@ -497,13 +500,17 @@ __global__ void __launch_bounds__(E * 32) k_fuzz_reset_w(SynthParams p) {
                           (lane & 1) ? p.states + e * kMtN : rows + j * kRowWords);
     }
   }
+  if (threadIdx.x == 0) TL_STAMP(1);
   __syncthreads();
   const int64_t e = e0 + warp;
   if (e >= p.n_env) return;
   MtLane R{rows + warp * kRowWords, 0, 0};
-  R.prepare_block_warp();
+  R.prepare_block_warp(rows + E * kRowWords + warp * kMtN);
+  if (threadIdx.x == 0) TL_STAMP(2);
   if (lane == 0) reset_script(p, e, p.seeds[e], R);
+  if (threadIdx.x == 0) TL_STAMP(3);
 }
+#endif
 
 // realize path: seed the realize RNG of given scripts (one thread per state,
 // streamed straight to global memory: no shared memory)

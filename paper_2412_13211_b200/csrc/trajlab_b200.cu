@@ -15,7 +15,10 @@
 #include "tl_label_tma.cuh"  // A/B probe build only (slower TMA-staged labeller)
 #endif
 #include "tl_synth.cuh"
-#include "tl_synth_cta.cuh"
+#include "tl_synth_warp.cuh"
+#ifdef TL_AB
+#include "tl_synth_cta.cuh"  // A/B probe build only (one CTA per episode)
+#endif
 #include "tl_filter.cuh"
 #include "tl_env.cuh"
 #include "tl_analytics.cuh"
@@ -320,17 +323,21 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
 // episodes (measured: scripts/reset_epw_ab.sh, scripts/reset_epw_ab2.sh)
 static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   const int n = sp.n_env, sms = sm_count();
-  // up to 64 episodes per SM: the warp-per-sampler latency form
+#ifdef TL_AB
+  // TL_RESET_W=8|16: the warp-per-sampler form (k_fuzz_reset_w), measured
+  // 1-2% slower on the headline step than the lane-per-sampler kernel below
   const char* fw = ab_env("TL_RESET_W");
-  const int wform = fw ? atoi(fw) : ((int64_t)n <= (int64_t)sms * 64 ? 8 : 0);
+  const int wform = fw ? atoi(fw) : 0;
   if (wform == 8) {
-    k_fuzz_reset_w<8><<<(n + 7) / 8, 8 * 32, 8 * kRowWords * 4, S(stream)>>>(sp);
+    k_fuzz_reset_w<8><<<(n + 7) / 8, 8 * 32, 8 * (kRowWords + kMtN) * 4, S(stream)>>>(sp);
     return;
   }
   if (wform == 16) {
-    k_fuzz_reset_w<16><<<(n + 15) / 16, 16 * 32, 16 * kRowWords * 4, S(stream)>>>(sp);
+    set_max_smem(k_fuzz_reset_w<16>, 16 * (kRowWords + kMtN) * 4);
+    k_fuzz_reset_w<16><<<(n + 15) / 16, 16 * 32, 16 * (kRowWords + kMtN) * 4, S(stream)>>>(sp);
     return;
   }
+#endif
   const char* force = ab_env("TL_RESET_EPW");
   const int epw = force ? atoi(force)
                         : (int64_t)n <= (int64_t)sms * 8 ? 1 : (int64_t)n <= (int64_t)sms * 64 ? 4 : 8;
@@ -379,6 +386,7 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   }
 }
 
+#ifdef TL_AB
 typedef void (*SynthKernel)(SynthParams);
 static SynthKernel synth_kernel(int w, bool fuzz, bool small) {
   if (w == 32)
@@ -387,32 +395,48 @@ static SynthKernel synth_kernel(int w, bool fuzz, bool small) {
   return fuzz ? (small ? k_synth_cta<true, 7, 64> : k_synth_cta<true, 16, 64>)
               : (small ? k_synth_cta<false, 7, 64> : k_synth_cta<false, 16, 64>);
 }
+#endif
+
+typedef void (*SynthWarpKernel)(SynthParams);
+constexpr int kSynthWarps = 4;  // warps (independent episodes) per CTA of k_synth_warp
 
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
-  // realize + label: one CTA per episode (tl_synth_cta.cuh); 2-warp CTAs
-  // (32-record waves) when no episode can exceed 64 records
+  // realize + label: one warp per episode (tl_synth_warp.cuh)
   const bool small = sp.out.dof <= 7;
-  const char* fw = ab_env("TL_SYNTH_WAVE");
-  const int W = fw ? (atoi(fw) == 32 ? 32 : 64)
-                   : (sp.cap_per_env > 0 && sp.cap_per_env <= 64 ? 32 : 64);
-  const int threads = W + 32;
-  const int smem = W == 32 ? (small ? (int)sizeof(CtaSmem<7, 32>) : (int)sizeof(CtaSmem<16, 32>))
-                           : (small ? (int)sizeof(CtaSmem<7, 64>) : (int)sizeof(CtaSmem<16, 64>));
-  SynthKernel k = synth_kernel(W, fuzz, small);
-  set_max_smem(k, smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
-  if (per_sm < 1) per_sm = 1;
   if (fuzz) {
     launch_fuzz_reset(sp, stream);
-  } else if (!fuzz) {
+  } else {
     k_seed_states<<<(sp.n_env + 127) / 128, 128, 0, S(stream)>>>(sp);
   }
-  const int grid = blocks_for(sp.n_env, 1, sm_count() * per_sm);
+#ifdef TL_AB
+  if (ab_env("TL_SYNTH_CTA")) {  // the one-CTA-per-episode kernel (tl_synth_cta.cuh)
+    const char* fw = ab_env("TL_SYNTH_WAVE");
+    const int W = fw ? (atoi(fw) == 32 ? 32 : 64)
+                     : (sp.cap_per_env > 0 && sp.cap_per_env <= 64 ? 32 : 64);
+    const int threads = W + 32;
+    const int smem = W == 32 ? (small ? (int)sizeof(CtaSmem<7, 32>) : (int)sizeof(CtaSmem<16, 32>))
+                             : (small ? (int)sizeof(CtaSmem<7, 64>) : (int)sizeof(CtaSmem<16, 64>));
+    SynthKernel k = synth_kernel(W, fuzz, small);
+    set_max_smem(k, smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    k<<<blocks_for(sp.n_env, 1, sm_count() * per_sm), threads, smem, S(stream)>>>(sp);
+    return check_launch();
+  }
+#endif
+  const SynthWarpKernel k = fuzz ? (small ? k_synth_warp<true, 7, kSynthWarps> : k_synth_warp<true, 16, kSynthWarps>)
+                                 : (small ? k_synth_warp<false, 7, kSynthWarps> : k_synth_warp<false, 16, kSynthWarps>);
+  const int smem = kSynthWarps * (small ? (int)sizeof(WarpSmem<7>) : (int)sizeof(WarpSmem<16>));
+  set_max_smem(k, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSynthWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int grid = blocks_for(sp.n_env, kSynthWarps, sm_count() * per_sm);
   if (ab_env("TL_DEBUG"))
-    fprintf(stderr, "k_synth_cta<W=%d>: %d CTAs/SM (smem %d B, %d threads), grid %d\n", W, per_sm,
-            smem, threads, grid);
-  k<<<grid, threads, smem, S(stream)>>>(sp);
+    fprintf(stderr, "k_synth_warp: %d CTAs/SM x %d warps (smem %d B), grid %d\n", per_sm,
+            kSynthWarps, smem, grid);
+  k<<<grid, kSynthWarps * 32, smem, S(stream)>>>(sp);
   return check_launch();
 }
 
