@@ -313,6 +313,99 @@ def eval_predicates(rb: RecordBatch, env_cset, csets, a0=None):
     return bits, errs, jmax
 
 
+class _OneRecord:
+    """tl_eval_predicates on ONE record for the scalar drop-in calls
+    (is_static, is_open, success_step, ... on a single TimestepRecord):
+    the record, its cset and the optional anchor are packed into a pinned
+    host staging block, then one H2D copy, one launch, one D2H copy of the
+    three outputs and one stream synchronize -- instead of a trajectory pack
+    (six copies) and three blocking reads per call.  The staging block and
+    the csets (keyed like CsetTable) are reused across calls."""
+
+    # byte layout of the staging block (8-byte aligned fields, cap = 4 records)
+    _CAP = 4
+    _PLANES = 0
+    _GRASPED = (2 * L.MAX_DOF + 9) * 4 * 8
+    _REC_START = _GRASPED + 8
+    _N_REC = _REC_START + 8
+    _ENV_CSET = _N_REC + 8
+    _A0 = _ENV_CSET + 8
+    _CSET = _A0 + 8
+    _SIZE = (_CSET + 512 + 255) & ~255
+
+    def __init__(self, dev):
+        torch = _torch()
+        self.host = torch.zeros(self._SIZE, dtype=torch.uint8, pin_memory=True)
+        self.dev = torch.zeros(self._SIZE, dtype=torch.uint8, device=dev)
+        self.out_dev = torch.zeros(64, dtype=torch.uint8, device=dev)
+        self.out_host = torch.zeros(64, dtype=torch.uint8, pin_memory=True)
+        self.h = self.host.numpy()
+        self.o = self.out_host.numpy()
+        self.csets = {}
+        base = self.dev.data_ptr()
+        self.p_planes = base + self._PLANES
+        self.p_grasped = base + self._GRASPED
+        self.p_rec_start = base + self._REC_START
+        self.p_n_rec = base + self._N_REC
+        self.p_env = base + self._ENV_CSET
+        self.p_a0 = base + self._A0
+        self.p_cset = base + self._CSET
+        ob = self.out_dev.data_ptr()
+        self.p_bits, self.p_errs, self.p_jmax = ob, ob + 8, ob + 32
+        self.h[self._REC_START:self._REC_START + 8] = np.zeros(1, np.int64).view(np.uint8)
+        self.h[self._N_REC:self._N_REC + 4] = np.ones(1, np.int32).view(np.uint8)
+        self.h[self._ENV_CSET:self._ENV_CSET + 4] = np.zeros(1, np.int32).view(np.uint8)
+
+    def cset(self, subtask, art_kind, qmin, qmax, dof, rest_arm, rest_tor, th) -> bytes:
+        key = (int(subtask), int(art_kind),
+               float(qmin).hex() if not math.isnan(qmin) else "nan",
+               float(qmax).hex() if not math.isnan(qmax) else "nan",
+               int(dof), tuple(float(v).hex() for v in rest_arm),
+               float(rest_tor).hex(), th.astuple())
+        b = self.csets.get(key)
+        if b is None:
+            b = cset_build(subtask, art_kind, qmin, qmax, dof, rest_arm, rest_tor, th)
+            self.csets[key] = b
+        return b
+
+    def eval(self, values, grasped: bool, dof: int, cset: bytes, a0=None):
+        """values: the 2*dof+9 record fields in plane order (f64) ->
+        (bits, errs, jmax) of the record."""
+        torch = _torch()
+        F = 2 * dof + 9
+        planes = self.h[self._PLANES:self._PLANES + F * self._CAP * 8].view(np.float64).reshape(F, self._CAP)
+        planes[:, 0] = values
+        self.h[self._GRASPED] = 1 if grasped else 0
+        self.h[self._A0:self._A0 + 8] = np.array([0.0 if a0 is None else a0], np.float64).view(np.uint8)
+        self.h[self._CSET:self._CSET + len(cset)] = np.frombuffer(cset, np.uint8)
+        stream = torch.cuda.current_stream()
+        self.dev.copy_(self.host, non_blocking=True)
+        rec = L.Records_c(self.p_planes, self.p_grasped, self.p_rec_start, self.p_n_rec,
+                          self._CAP, 1, int(dof))
+        rc = L.lib().tl_eval_predicates(ctypes.byref(rec), 1, ctypes.c_void_p(self.p_env),
+                                        ctypes.c_void_p(self.p_cset),
+                                        None if a0 is None else ctypes.c_void_p(self.p_a0),
+                                        ctypes.c_void_p(self.p_bits), ctypes.c_void_p(self.p_errs),
+                                        ctypes.c_void_p(self.p_jmax),
+                                        ctypes.c_void_p(stream.cuda_stream))
+        L.check(rc, "tl_eval_predicates")
+        self.out_host.copy_(self.out_dev, non_blocking=True)
+        stream.synchronize()
+        return int(self.o[0]), int(self.o[8]), float(self.o[32:40].view(np.float64)[0])
+
+
+_one = {}
+
+
+def one_record():
+    """The per-device _OneRecord staging (created on first use)."""
+    dev = L.device()
+    r = _one.get(dev.index)
+    if r is None:
+        r = _one[dev.index] = _OneRecord(dev)
+    return r
+
+
 def classify_lists(kinds_list, subtasks, d0s, d0_none, rules=None):
     """tl_classify_events over host event lists -> numpy tl_label array."""
     torch = _torch()

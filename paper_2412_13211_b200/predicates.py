@@ -10,7 +10,7 @@ import math
 
 from . import core
 from .errors import MissingArticulation, RequiredFieldNaN
-from .model import SUBTASK_ORDER, ART_ORDER, SubtaskKind, TimestepRecord, Trajectory, TrajectoryHeader
+from .model import SUBTASK_ORDER, ART_ORDER, SCALAR_FIELDS, SubtaskKind, TimestepRecord, Trajectory, TrajectoryHeader
 from .thresholds import Thresholds
 
 _B_CONTACT, _B_GRASP, _B_SUCC, _B_CUM_LE, _B_CUM_GT, _B_A, _B_B, _B_STATIC = (
@@ -28,22 +28,19 @@ def _blank(dof, **kw):
 
 
 def _eval(rec, hdr, th, subtask=None, a0=None):
-    """(bits, errs, jmax) of one record under hdr/th (subtask overridable)."""
-    h = hdr
-    if subtask is not None and subtask != hdr.subtask_kind:
-        h = TrajectoryHeader(episode_id="", subtask_kind=subtask,
-                             articulation_kind=hdr.articulation_kind,
-                             art_qmin=hdr.art_qmin, art_qmax=hdr.art_qmax,
-                             arm_dof=hdr.arm_dof, rest_arm=hdr.rest_arm,
-                             rest_tor=hdr.rest_tor)
-    t = Trajectory(header=TrajectoryHeader(
-        episode_id="", subtask_kind=h.subtask_kind, articulation_kind=h.articulation_kind,
-        art_qmin=h.art_qmin, art_qmax=h.art_qmax, arm_dof=h.arm_dof,
-        rest_arm=h.rest_arm, rest_tor=h.rest_tor, thresholds_override=th),
-        records=[rec])
-    rb, env, cs, _ = core.pack_trajectories([t], th, force_f64=True)
-    bits, errs, jmax = core.eval_predicates(rb, env, cs, None if a0 is None else [a0])
-    return int(bits[0].item()), int(errs[0].item()), float(jmax[0].item())
+    """(bits, errs, jmax) of one record under hdr/th (subtask overridable):
+    one staged launch (core.one_record)."""
+    dof = hdr.arm_dof
+    if len(rec.q_arm) != dof or len(rec.qd_arm) != dof:
+        raise ValueError(f"joint vector length mismatch: {len(rec.q_arm)} vs {dof}")
+    if len(hdr.rest_arm) != dof:
+        raise ValueError(f"joint vector length mismatch: {dof} vs {len(hdr.rest_arm)}")
+    sub = hdr.subtask_kind if subtask is None else subtask
+    one = core.one_record()
+    cs = one.cset(SUBTASK_ORDER.index(sub), ART_ORDER.index(hdr.articulation_kind),
+                  hdr.art_qmin, hdr.art_qmax, dof, hdr.rest_arm, hdr.rest_tor, th)
+    values = [*rec.q_arm, *rec.qd_arm, *(getattr(rec, f) for f in SCALAR_FIELDS)]
+    return one.eval(values, rec.grasped, dof, cs, a0)
 
 
 def j_max(q, r) -> float:
