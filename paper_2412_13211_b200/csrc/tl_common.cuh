@@ -349,6 +349,16 @@ __device__ __forceinline__ double rand53(uint32_t w0, uint32_t w1) {
   return k ? r : 0.0;
 }
 
+// a + span * random() for the 53-bit k of words (w0, w1), given span_s =
+// span * 2^-53: span * (k * 2^-53) and span_s * k are the same real number,
+// so the rounded product (and sum) equal CPython's uniform(a, a + span)
+__device__ __forceinline__ double uniform_k53(double a, double span_s, uint32_t w0, uint32_t w1) {
+  const uint32_t hi = w0 >> 11;
+  const uint32_t lo = __funnelshift_r(w1, w0 >> 5, 6);  // ((w0 >> 5) << 26) | (w1 >> 6)
+  const double k = __ull2double_rn(((uint64_t)hi << 32) | lo);
+  return __dadd_rn(a, __dmul_rn(span_s, k));
+}
+
 // cp.async (global -> shared, no registers in flight)
 __device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);

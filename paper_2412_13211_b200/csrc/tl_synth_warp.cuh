@@ -29,6 +29,9 @@ struct WarpCfg {
   static constexpr int kRing = DOFMAX <= 7 ? 2048 : 4096;
   static_assert(kRing >= 32 * (4 + 2 * (2 * DOFMAX + 5)) + 623, "ring too small");
   static constexpr uint32_t kMask = kRing - 1;
+  // the ring's first kApron words are mirrored past its end, so one record's
+  // 2*(2*dof+5) emit words are contiguous from any start (no wrap per draw)
+  static constexpr int kApron = (2 * (2 * DOFMAX + 5) + 3) & ~3;
   static constexpr int kSteps = 32;  // script steps planned per window
 };
 
@@ -36,7 +39,7 @@ template <int DOFMAX>
 struct WarpSmem {
   static constexpr int kSteps = WarpCfg<DOFMAX>::kSteps;
   alignas(16) uint32_t mt[kMtN];                       // MT state, regenerated in place
-  alignas(16) uint32_t wb[WarpCfg<DOFMAX>::kRing];     // tempered words
+  alignas(16) uint32_t wb[WarpCfg<DOFMAX>::kRing + WarpCfg<DOFMAX>::kApron];  // tempered words
   int32_t gap[kSteps];
   int32_t tau[kSteps];
   int32_t W[kSteps + 1];
@@ -66,10 +69,14 @@ __device__ __forceinline__ void twist_phase_warp(uint32_t* mt, uint32_t* ring, u
     if (g < G1) {
       const uint4 cur = reinterpret_cast<const uint4*>(mt)[g];
       const int i = 4 * g;
-      const uint32_t nxt = mt[i + 4 == kMtN ? 0 : i + 4];
-      auto src = [&](int k) {
+      uint32_t nxt;
+      if constexpr (G1 * 4 == kMtN) nxt = mt[i + 4 == kMtN ? 0 : i + 4];
+      else nxt = mt[i + 4];
+      auto src = [&](int k) {  // phases 1 and 3 lie wholly on one side of word 227
         const int ii = i + k;
-        return mt[ii < kMtN - kMtM ? ii + kMtM : ii - (kMtN - kMtM)];
+        if constexpr (G1 * 4 <= kMtN - kMtM) return mt[ii + kMtM];
+        else if constexpr (G0 * 4 >= kMtN - kMtM) return mt[ii - (kMtN - kMtM)];
+        else return mt[ii < kMtN - kMtM ? ii + kMtM : ii - (kMtN - kMtM)];
       };
       nv[q].x = mt_mix(cur.x, cur.y, src(0));
       nv[q].y = mt_mix(cur.y, cur.z, src(1));
@@ -85,7 +92,10 @@ __device__ __forceinline__ void twist_phase_warp(uint32_t* mt, uint32_t* ring, u
       reinterpret_cast<uint4*>(mt)[g] = nv[q];
       const uint4 tv = make_uint4(mt_temper(nv[q].x), mt_temper(nv[q].y), mt_temper(nv[q].z),
                                   mt_temper(nv[q].w));
-      reinterpret_cast<uint4*>(ring)[((base + 4u * g) & kMask) >> 2] = tv;
+      const uint32_t at = (base + 4u * g) & kMask;
+      reinterpret_cast<uint4*>(ring)[at >> 2] = tv;
+      if (at < (uint32_t)WarpCfg<DOFMAX>::kApron)
+        reinterpret_cast<uint4*>(ring)[(WarpCfg<DOFMAX>::kRing + at) >> 2] = tv;
     }
   }
   __syncwarp();
@@ -340,11 +350,15 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
           const StepSt stv = S.st[sidx];
           const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
           float* __restrict__ dst = P + rr;
-          // branch-free: every draw is computed, at-rest records select 0
-          // rng.uniform(a, b) with b - a folded at compile time (same RN result)
-          auto draw = [&](uint32_t k, double a, double span) -> float {
-            const uint2 wv = ring2[((eo + 2u * k) & kMask) >> 1];
-            const float v = __double2float_rn(uniform_span(a, span, rand53(wv.x, wv.y)));
+          // branch-free: every draw is computed, at-rest records select 0.
+          // The record's emit words are contiguous in the ring (apron), and
+          // rng.uniform(a, b) = a + (b - a) * (k * 2^-53) is evaluated as
+          // a + ((b - a) * 2^-53) * k: the same real product, so the same
+          // rounding, with the scaled span folded at compile time
+          const uint2* rw = ring2 + ((eo & kMask) >> 1);
+          auto draw = [&](const uint2* w, double a, double span) -> float {
+            const uint2 wv = *w;
+            const float v = __double2float_rn(uniform_k53(a, span * 0x1.0p-53, wv.x, wv.y));
             return emit ? v : 0.f;
           };
           RecV<float> v;
@@ -352,7 +366,7 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
 #pragma unroll
           for (int i = 0; i < DOFMAX; i++) {
             if (i < dof) {
-              const float q = draw(i, -0.3, 0.3 - -0.3);
+              const float q = draw(rw + i, -0.3, 0.3 - -0.3);
               *dst = q;
               dst += stride;
               mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
@@ -361,18 +375,18 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
 #pragma unroll
           for (int i = 0; i < DOFMAX; i++) {
             if (i < dof) {
-              const float qd = draw(dof + i, -0.4, 0.4 - -0.4);
+              const float qd = draw(rw + dof + i, -0.4, 0.4 - -0.4);
               *dst = qd;
               dst += stride;
               mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
             }
           }
-          const uint32_t k2 = 2 * dof;
-          v.tor = draw(k2, -0.05, 0.05 - -0.05);
-          v.vx = draw(k2 + 1, -0.2, 0.2 - -0.2);
-          v.vy = draw(k2 + 2, -0.2, 0.2 - -0.2);
-          v.om = draw(k2 + 3, -0.3, 0.3 - -0.3);
-          v.der = draw(k2 + 4, 0.2, 1.0 - 0.2);
+          const uint2* r2 = rw + 2 * dof;
+          v.tor = draw(r2, -0.05, 0.05 - -0.05);
+          v.vx = draw(r2 + 1, -0.2, 0.2 - -0.2);
+          v.vy = draw(r2 + 2, -0.2, 0.2 - -0.2);
+          v.om = draw(r2 + 3, -0.3, 0.3 - -0.3);
+          v.der = draw(r2 + 4, 0.2, 1.0 - 0.2);
           v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
           v.force = stv.force;
           v.cum = 0.f;  // over = false here; cum_patch_bits applies the real value
