@@ -865,7 +865,7 @@ def main(argv=None):
         synth_ms = [a.elapsed_time(b) for a, b in kev]
 
         # ---- end to end through the C ABI with host buffers (wall clock) ---
-        # E: pinned host seeds -> GPU (H2D), the fused kernels write the event
+        # E: pinned host seeds -> GPU (H2D), k_scan_emit writes the event
         # lists into pinned host memory (zero-copy), labels come back by a D2H
         # copy (N>1: after the NCCL all-gather + histogram, which also comes
         # back); perf_counter around call + synchronize, per step.
@@ -973,13 +973,13 @@ def main(argv=None):
         "trajectories_per_sec": N_ENV * world * K / t_dev,
         "config": bench_config(world),
         "mean_steps_per_episode": recs_per_launch / N_ENV,
-        "step": "1 CUDA graph: tl_fuzz_ev (k_fuzz_reset + k_synth_cta, which also emits the ordered "
-                "event lists)" + (", NCCL all_gather of the labels + tl_mode_histogram of the "
+        "step": "1 CUDA graph: tl_fuzz_ev (k_fuzz_reset, k_synth_warp: realize + labels, "
+                "k_scan_emit: ordered event lists)" + (", NCCL all_gather of the labels + tl_mode_histogram of the "
                                   "gathered labels" if world > 1 else ""),
         "timing": "CUDA events per step on the launch stream, max over ranks",
         "gpu_launches": launches_per_step * K,
         "roofline": {
-            "kernel": "k_fuzz_reset + k_synth_cta (tl_fuzz_ev)", "bound": "latency",
+            "kernel": "k_fuzz_reset + k_synth_warp + k_scan_emit (tl_fuzz_ev)", "bound": "latency",
             "achieved": crit_cycles / step_s / 1e9, "peak": sm_ghz,
             "unit": "GHz (critical-path cycles retired per second vs the SM clock)",
             "frac": floor_s / step_s,

@@ -111,21 +111,25 @@ __device__ __forceinline__ bool in_alpha(int k, int ev) {
 }
 
 // choices(pop, weights)[0] (Lib/random.py): accumulate + bisect_right
-__device__ int choices_idx(MtLane& R, const double* w, int n) {
-  double cum[4];
-  double acc = 0.0;
-  for (int i = 0; i < n; i++) {
-    acc = i == 0 ? w[0] : __dadd_rn(acc, w[i]);
+// (N is a compile-time population size: the cumulative weights stay in
+// registers)
+template <int N>
+__device__ __forceinline__ int choices_idx(MtLane& R, const double (&w)[N]) {
+  double cum[N];
+  double acc = w[0];
+  cum[0] = acc;
+#pragma unroll
+  for (int i = 1; i < N; i++) {
+    acc = __dadd_rn(acc, w[i]);
     cum[i] = acc;
   }
-  const double total = __dadd_rn(cum[n - 1], 0.0);
+  const double total = __dadd_rn(cum[N - 1], 0.0);
   const double x = __dmul_rn(R.random(), total);
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (x < cum[mid]) hi = mid; else lo = mid + 1;
-  }
-  return lo;
+  int idx = N - 1;  // bisect_right over cum[0..N-2]: the first i with x < cum[i]
+#pragma unroll
+  for (int i = N - 2; i >= 0; i--)
+    if (x < cum[i]) idx = i;
+  return idx;
 }
 
 // random_script (synth.py:363-507), one thread.  Returns n_steps, or -1
@@ -157,7 +161,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
     sc.initial_dist_obj_goal = R.random() < 0.7 ? R.uniform(0.3, 0.9) : R.uniform(0.02, 0.12);
   } else {                                                               // :387-392
     const double w[3] = {0.85, 0.1, 0.05};
-    const int c = choices_idx(R, w, 3);
+    const int c = choices_idx(R, w);
     if (kind == TL_OPEN) sc.initial_level = c == 0 ? TL_LVL_LOW : c == 1 ? TL_LVL_SLIGHT : TL_LVL_OPEN;
     else sc.initial_level = c == 0 ? TL_LVL_HIGH : c == 1 ? TL_LVL_SLIGHT : TL_LVL_CLOSED;
   }
@@ -172,30 +176,29 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
   bool contact_used = contact;                                           // :461
   const long n_target = (long)rint(__dmul_rn((double)R.randint(0, cfg.max_events), cfg.edge_density));
   for (long it = 0; it < n_target; it++) {                               // :464-474
-    int mv[3], nm = 0;
+    // the legal moves (at most 3), packed one byte each into a register
+    // (no local-memory array): move i = (mv >> 8i) & 0xff
+    uint32_t mv = 0;
+    int nm = 0;
+    auto add = [&](int ev) { mv |= (uint32_t)ev << (8 * nm); nm++; };
     if (kind == TL_PICK) {
-      if (!contact) mv[nm++] = TL_EV_CONTACT;
-      if (!grasped && contact) mv[nm++] = TL_EV_GRASPED;
-      if (grasped) mv[nm++] = TL_EV_DROPPED;
+      if (!contact) add(TL_EV_CONTACT);
+      if (!grasped && contact) add(TL_EV_GRASPED);
+      if (grasped) add(TL_EV_DROPPED);
     } else if (kind == TL_PLACE) {
-      mv[nm++] = !grasped ? TL_EV_GRASPED : in_goal ? TL_EV_RELEASED_AT_GOAL : TL_EV_RELEASED_OUTSIDE_GOAL;
-      mv[nm++] = in_goal ? TL_EV_OBJ_LEFT_GOAL : TL_EV_OBJ_AT_GOAL;
+      add(!grasped ? TL_EV_GRASPED : in_goal ? TL_EV_RELEASED_AT_GOAL : TL_EV_RELEASED_OUTSIDE_GOAL);
+      add(in_goal ? TL_EV_OBJ_LEFT_GOAL : TL_EV_OBJ_AT_GOAL);
     } else if (kind == TL_OPEN) {
-      mv[nm++] = TL_EV_CONTACT;
-      mv[nm++] = level == TL_LVL_LOW ? TL_EV_SLIGHTLY_OPENED : level == TL_LVL_SLIGHT ? TL_EV_OPENED : TL_EV_CLOSED;
+      if (!contact_used) add(TL_EV_CONTACT);  // Contact is dropped once used (:416-419)
+      add(level == TL_LVL_LOW ? TL_EV_SLIGHTLY_OPENED : level == TL_LVL_SLIGHT ? TL_EV_OPENED : TL_EV_CLOSED);
     } else {
-      mv[nm++] = TL_EV_CONTACT;
-      if (level == TL_LVL_OPEN) { if (band) mv[nm++] = TL_EV_SLIGHTLY_CLOSED; }
-      else if (level == TL_LVL_SLIGHT) mv[nm++] = TL_EV_CLOSED;
-      else mv[nm++] = TL_EV_OPEN;
-    }
-    if ((kind == TL_OPEN || kind == TL_CLOSE) && contact_used) {
-      int k = 0;
-      for (int i = 0; i < nm; i++) if (mv[i] != TL_EV_CONTACT) mv[k++] = mv[i];
-      nm = k;
+      if (!contact_used) add(TL_EV_CONTACT);
+      if (level == TL_LVL_OPEN) { if (band) add(TL_EV_SLIGHTLY_CLOSED); }
+      else if (level == TL_LVL_SLIGHT) add(TL_EV_CLOSED);
+      else add(TL_EV_OPEN);
     }
     if (!nm) break;
-    const int m = mv[R.randbelow((uint32_t)nm)];
+    const int m = (int)((mv >> (8 * R.randbelow((uint32_t)nm))) & 0xffu);
     if (m == TL_EV_CONTACT) contact_used = true;
     push(m);
     switch (m) {                                                         // :434-457
@@ -221,7 +224,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
   if (want && feasible) {
     push(TL_EV_SUCCESS);
     const double w[4] = {0.55, 0.2, 0.15, kind == TL_PLACE ? 0.1 : 0.0};
-    const int suffix = choices_idx(R, w, 4);
+    const int suffix = choices_idx(R, w);
     if (suffix == 1) {
       // the dict literal at :493-496 evaluates gap() for all four subtasks
       int32_t g[4];
@@ -511,6 +514,47 @@ __global__ void __launch_bounds__(E * 32) k_fuzz_reset_w(SynthParams p) {
   if (threadIdx.x == 0) TL_STAMP(3);
 }
 #endif
+
+// The same with both states streamed into shared rows 2j / 2j+1 (every
+// seeding store is a shared-space store: no generic stores splitting
+// between shared and global memory inside the 624-step loops), then the warp
+// copies the realize rows to global memory, coalesced, while nothing else
+// waits on them; the even lanes then sample random_script.
+template <int EPW>
+__global__ void __launch_bounds__(32) k_fuzz_reset_sh(SynthParams p) {
+  extern __shared__ uint32_t rows[];  // [2*EPW][kRowWords]
+  const int lane = lane_id();
+  const int64_t e0 = (int64_t)blockIdx.x * EPW;
+  const int64_t e = e0 + (lane >> 1);
+  const bool valid = (lane >> 1) < EPW && e < p.n_env;
+  uint32_t* row = rows + (lane < 2 * EPW ? lane : 0) * kRowWords;
+  if (lane == 0) TL_STAMP(0);
+  if (blockIdx.x == 0 && lane == 0 && p.tickets) reset_counters(p);
+  int64_t seed = 0;
+  if (valid) {
+    seed = p.seeds[e];
+    const int64_t s = (lane & 1) ? (seed ^ 0x5EED) : seed;
+    const uint64_t n = s < 0 ? (uint64_t)0 - (uint64_t)s : (uint64_t)s;
+    const uint32_t k0 = (uint32_t)n, k1 = (uint32_t)(n >> 32);
+    if (k1) mt_seed_stream_impl<2>(k0, k1, row);
+    else mt_seed_stream_impl<1>(k0, 0u, row);
+  }
+  __syncwarp();
+  if (lane == 0) TL_STAMP(1);
+  const int ne = (int)min((int64_t)EPW, (int64_t)p.n_env - e0);
+  for (int q = 0; q < ne; q++) {
+    const uint32_t* src = rows + (2 * q + 1) * kRowWords;
+    uint32_t* dst = p.states + (e0 + q) * kMtN;
+#pragma unroll 4
+    for (int i = lane; i < kMtN; i += 32) dst[i] = src[i];
+  }
+  if (valid && !(lane & 1)) {
+    MtLane R{row, 0, 0};
+    R.prepare(128);
+    reset_script(p, e, seed, R);
+  }
+  if (lane == 0) TL_STAMP(2);
+}
 
 // realize path: seed the realize RNG of given scripts (one thread per state,
 // streamed straight to global memory: no shared memory)

@@ -92,10 +92,7 @@ __device__ __forceinline__ void twist_phase_warp(uint32_t* mt, uint32_t* ring, u
       reinterpret_cast<uint4*>(mt)[g] = nv[q];
       const uint4 tv = make_uint4(mt_temper(nv[q].x), mt_temper(nv[q].y), mt_temper(nv[q].z),
                                   mt_temper(nv[q].w));
-      const uint32_t at = (base + 4u * g) & kMask;
-      reinterpret_cast<uint4*>(ring)[at >> 2] = tv;
-      if (at < (uint32_t)WarpCfg<DOFMAX>::kApron)
-        reinterpret_cast<uint4*>(ring)[(WarpCfg<DOFMAX>::kRing + at) >> 2] = tv;
+      reinterpret_cast<uint4*>(ring)[((base + 4u * g) & kMask) >> 2] = tv;
     }
   }
   __syncwarp();
@@ -106,6 +103,14 @@ __device__ __forceinline__ void twist_block_warp(uint32_t* mt, uint32_t* ring, u
   twist_phase_warp<DOFMAX, 0, 56>(mt, ring, base);     // words 0..223: old words only
   twist_phase_warp<DOFMAX, 56, 112>(mt, ring, base);   // 224..447: new 0..220
   twist_phase_warp<DOFMAX, 112, 156>(mt, ring, base);  // 448..623: new 221..396, word 0
+  // the block rewrote ring words [0, kApron): refresh their mirror
+  constexpr int kRing = WarpCfg<DOFMAX>::kRing, kApron = WarpCfg<DOFMAX>::kApron;
+  const uint32_t b0 = base & WarpCfg<DOFMAX>::kMask;
+  if (b0 < (uint32_t)kApron || b0 + kMtN > (uint32_t)kRing) {  // warp-uniform
+    if (lane_id() < kApron / 4)
+      reinterpret_cast<uint4*>(ring)[kRing / 4 + lane_id()] = reinterpret_cast<const uint4*>(ring)[lane_id()];
+    __syncwarp();
+  }
 }
 
 // longest-first claims (see claim_episode): lane b < 16 holds the exclusive

@@ -338,6 +338,22 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
     return;
   }
 #endif
+  if (ab_env("TL_RESET_SH")) {
+    const int e = atoi(ab_env("TL_RESET_SH"));
+    const int smem = 2 * e * kRowWords * 4;
+    if (e == 4) {
+      set_max_smem(k_fuzz_reset_sh<4>, smem);
+      k_fuzz_reset_sh<4><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
+    } else if (e == 2) {
+      k_fuzz_reset_sh<2><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
+    } else if (e == 8) {
+      set_max_smem(k_fuzz_reset_sh<8>, smem);
+      k_fuzz_reset_sh<8><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
+    } else {
+      k_fuzz_reset_sh<1><<<n, 32, smem, S(stream)>>>(sp);
+    }
+    return;
+  }
   const char* force = ab_env("TL_RESET_EPW");
   const int epw = force ? atoi(force)
                         : (int64_t)n <= (int64_t)sms * 8 ? 1 : (int64_t)n <= (int64_t)sms * 64 ? 4 : 8;
