@@ -15,7 +15,9 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "libtrajlab_b200.so")
+# TRAJLAB_B200_LIB selects another build of the same library (the checked
+# build of scripts/gpu_check_build.sh); default: the in-tree product build
+LIB_PATH = os.environ.get("TRAJLAB_B200_LIB") or os.path.join(PKG, "libtrajlab_b200.so")
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 

@@ -10,6 +10,7 @@
 // intrinsics (and the library is built with -fmad=false): no contraction.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "../../include/trajlab_b200.h"
@@ -23,6 +24,24 @@ __device__ unsigned long long g_tl_prof[128];
 #define TL_STAMP(i) do { if (blockIdx.x == 0) g_tl_prof[(i)] = clock64(); } while (0)
 #else
 #define TL_STAMP(i) do { } while (0)
+#endif
+
+// Bounds / invariant checks of the checked build (-DTL_CHECK,
+// scripts/gpu_check_build.sh): a failing check prints its site and traps
+// (the CUDA context dies, the calling test fails loudly).  compute-sanitizer
+// is not available on the GPU pool, so this build + the GPU test suite is
+// the memory-safety evidence; the product build compiles them out.
+#ifdef TL_CHECK
+#define TL_ASSERT(c)                                                              \
+  do {                                                                            \
+    if (!(c)) {                                                                   \
+      printf("TL_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                  \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define TL_ASSERT(c) do { } while (0)
 #endif
 
 constexpr int kWarp = 32;

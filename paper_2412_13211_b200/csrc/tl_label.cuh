@@ -941,6 +941,7 @@ __global__ void __launch_bounds__(kLabelWarps * 32, PART == 1 ? TL_LABEL_MINB : 
            vec_ok && rs + (((int64_t)n + 3) & ~(int64_t)3) <= stride && csets[ci].rest_zero;
   };
   auto process = [&](int e, int ci, int64_t rs, int n) {
+    TL_ASSERT(rs >= 0 && n >= 0 && rs + n <= R.plane_stride && ci >= 0);
     stage_cset(&s_cs[warp], &csets[ci]);
     const tl_cset& c = s_cs[warp];
     LState S;
@@ -1186,6 +1187,7 @@ __global__ void __launch_bounds__(kLabelWarps * 32)
     const tl_cset& c = s_cs[warp];
     const int64_t rs = R.rec_start[e];
     const int n = R.n_rec[e];
+    TL_ASSERT(rs >= 0 && n >= 0 && rs + n <= R.plane_stride);
     float sc_ru = 0.f;
     double sc_d = 0.0;
     if (c.subtask == TL_CLOSE && n > 0)
@@ -1264,6 +1266,7 @@ __global__ void __launch_bounds__(256)
   for (int e = blockIdx.x * 8 + warp; e < n_env; e += gridDim.x * 8) {
     const int64_t a = src.rec_start[e], b = dst_start[e];
     const int n = src.n_rec[e];
+    TL_ASSERT(a >= 0 && n >= 0 && a + n <= src.plane_stride && b >= 0 && b + n <= dst.plane_stride);
     for (int t = lane; t < n; t += 32) {
       for (int f = 0; f < n_planes; f++) dp[f * dst.plane_stride + b + t] = sp[f * src.plane_stride + a + t];
       dst.grasped[b + t] = src.grasped[a + t];
@@ -1349,6 +1352,7 @@ __global__ void __launch_bounds__(1024)
   const int sub = labels[e].subtask;
   const int64_t rs = rec_start[e];
   const int n = n_rec[e];
+  TL_ASSERT(rs >= 0 && n >= 0);
   int64_t base = s_off[warp];
   // four records per lane (one 32-bit load when the episode's masks are
   // 4-byte aligned), up to eight 128-record chunks loaded before any is

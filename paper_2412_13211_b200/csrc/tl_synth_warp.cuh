@@ -177,6 +177,8 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
     }
     const int64_t rs = p.out.rec_start[e];
     const int n_rec = p.out.n_rec[e];
+    TL_ASSERT(rs >= 0 && n_rec >= 0 && rs + n_rec <= p.out.plane_stride);
+    TL_ASSERT(!FUZZ || n_rec <= p.cap_per_env);
     {
       const uint4* src = reinterpret_cast<const uint4*>(p.states + (int64_t)e * kMtN);
       __syncwarp();  // the previous episode is done with S.mt
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
           }
         }
         seg_hint = __shfl_sync(kFull, s, 0);  // lane 0 holds the wave's first record
+        TL_ASSERT(!valid || (r < n_rec && s <= ns && sidx <= ns));
         const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
         const int need_max = __reduce_max_sync(kFull, need);
         while ((int)produced < need_max) {
@@ -317,7 +320,10 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
           return rand53(wv.x, wv.y);
         };
         S.radv[lane] = valid && adv ? rnd(o) : 0.0;
+        TL_ASSERT(!(valid && adv) || ((uint32_t)o + 2u <= produced &&
+                                      produced - (uint32_t)o <= (uint32_t)WarpCfg<DOFMAX>::kRing));
         if (valid && app) {
+          TL_ASSERT(s < ns);
           const double rr = rnd(o + 2 * adv);
           S.dist_after[s] = ev == TL_EV_OBJ_AT_GOAL ? TL_UNIFORM(0.02, 0.12, rr) : TL_UNIFORM(0.3, 0.8, rr);
         }
@@ -361,6 +367,10 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
           // a + ((b - a) * 2^-53) * k: the same real product, so the same
           // rounding, with the scaled span folded at compile time
           const uint2* rw = ring2 + ((eo & kMask) >> 1);
+          TL_ASSERT(!emit || (eo + 2u * (2 * dof + 5) <= produced &&
+                              produced - eo <= (uint32_t)WarpCfg<DOFMAX>::kRing &&
+                              (eo & kMask) + 2u * (2 * dof + 5) <=
+                                  (uint32_t)(WarpCfg<DOFMAX>::kRing + WarpCfg<DOFMAX>::kApron)));
           auto draw = [&](const uint2* w, double a, double span) -> float {
             const uint2 wv = *w;
             const float v = __double2float_rn(uniform_k53(a, span * 0x1.0p-53, wv.x, wv.y));

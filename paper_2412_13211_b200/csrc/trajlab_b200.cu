@@ -316,11 +316,10 @@ int tl_classify_events(const uint8_t* ev_kind, const int64_t* ev_off, const uint
   return check_launch();
 }
 
-// k_fuzz_reset with EPW episodes per warp (2*EPW seeding lanes): one
-// episode per warp while that keeps <= 8 warps per SM, 4 up to 64 episodes
-// per SM, else 8 -- the seeding chains are latency-bound and more warps
-// contend for issue, while the sampler is branchy code that diverges across
-// episodes (measured: scripts/reset_epw_ab.sh, scripts/reset_epw_ab2.sh)
+// fuzz reset shape by batch size: the seeding chains are latency-bound and
+// more warps contend for issue, while the sampler is branchy code that
+// diverges across the episodes of a warp (measured: scripts/reset_epw_ab*.sh,
+// scripts/ab_env.sh; the A/B build keeps the other shapes behind env knobs)
 static void launch_fuzz_reset(SynthParams& sp, void* stream) {
   const int n = sp.n_env, sms = sm_count();
 #ifdef TL_AB
@@ -337,7 +336,6 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
     k_fuzz_reset_w<16><<<(n + 15) / 16, 16 * 32, 16 * (kRowWords + kMtN) * 4, S(stream)>>>(sp);
     return;
   }
-#endif
   if (ab_env("TL_RESET_SH")) {
     const int e = atoi(ab_env("TL_RESET_SH"));
     const int smem = 2 * e * kRowWords * 4;
@@ -346,59 +344,39 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
       k_fuzz_reset_sh<4><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
     } else if (e == 2) {
       k_fuzz_reset_sh<2><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
-    } else if (e == 8) {
+    } else {
       set_max_smem(k_fuzz_reset_sh<8>, smem);
       k_fuzz_reset_sh<8><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
-    } else {
-      k_fuzz_reset_sh<1><<<n, 32, smem, S(stream)>>>(sp);
     }
     return;
   }
-  const char* force = ab_env("TL_RESET_EPW");
-  const int epw = force ? atoi(force)
-                        : (int64_t)n <= (int64_t)sms * 8 ? 1 : (int64_t)n <= (int64_t)sms * 64 ? 4 : 8;
-  // large batches: streamed seeding, one shared-memory row per episode
-  const bool stream_seed = epw >= 2 && ab_env("TL_RESET_ROWS2") == nullptr;
-  const int smem = (stream_seed ? 1 : 2) * epw * kRowWords * 4;
-  switch (epw) {
-    case 1: k_fuzz_reset<1, false><<<n, 32, smem, S(stream)>>>(sp); break;
-    case 2:
-      if (stream_seed) {
-        set_max_smem(k_fuzz_reset<2, true>, smem);
-        k_fuzz_reset<2, true><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
-      } else {
-        set_max_smem(k_fuzz_reset<2, false>, smem);
-        k_fuzz_reset<2, false><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp);
-      }
-      break;
-    case 4:
-      if (stream_seed) {
-        set_max_smem(k_fuzz_reset<4, true>, smem);
-        k_fuzz_reset<4, true><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
-      } else {
-        set_max_smem(k_fuzz_reset<4, false>, smem);
-        k_fuzz_reset<4, false><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp);
-      }
-      break;
-    case 8:
-      if (stream_seed) {
-        set_max_smem(k_fuzz_reset<8, true>, smem);
-        k_fuzz_reset<8, true><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
-      } else {
-        set_max_smem(k_fuzz_reset<8, false>, smem);
-        k_fuzz_reset<8, false><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp);
-      }
-      break;
-    default: {
-      const int sm16 = (stream_seed ? 1 : 2) * 16 * kRowWords * 4;
-      if (stream_seed) {
-        set_max_smem(k_fuzz_reset<16, true>, sm16);
-        k_fuzz_reset<16, true><<<(n + 15) / 16, 32, sm16, S(stream)>>>(sp);
-      } else {
-        set_max_smem(k_fuzz_reset<16, false>, sm16);
-        k_fuzz_reset<16, false><<<(n + 15) / 16, 32, sm16, S(stream)>>>(sp);
-      }
-    }
+  if (const char* force = ab_env("TL_RESET_EPW")) {
+    const int epw = atoi(force);
+    const bool stream_seed = epw >= 2 && ab_env("TL_RESET_ROWS2") == nullptr;
+    const int smem = (stream_seed ? 1 : 2) * epw * kRowWords * 4;
+    if (epw == 2 && stream_seed) { set_max_smem(k_fuzz_reset<2, true>, smem); k_fuzz_reset<2, true><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp); }
+    else if (epw == 2) { set_max_smem(k_fuzz_reset<2, false>, smem); k_fuzz_reset<2, false><<<(n + 1) / 2, 32, smem, S(stream)>>>(sp); }
+    else if (epw == 4 && stream_seed) { set_max_smem(k_fuzz_reset<4, true>, smem); k_fuzz_reset<4, true><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp); }
+    else if (epw == 4) { set_max_smem(k_fuzz_reset<4, false>, smem); k_fuzz_reset<4, false><<<(n + 3) / 4, 32, smem, S(stream)>>>(sp); }
+    else if (epw == 16) { set_max_smem(k_fuzz_reset<16, true>, smem); k_fuzz_reset<16, true><<<(n + 15) / 16, 32, smem, S(stream)>>>(sp); }
+    else { set_max_smem(k_fuzz_reset<8, true>, smem); k_fuzz_reset<8, true><<<(n + 7) / 8, 32, smem, S(stream)>>>(sp); }
+    return;
+  }
+#endif
+  if ((int64_t)n <= (int64_t)sms * 8) {
+    // one episode per warp: the sampler is serial branchy code that diverges
+    // across episodes; one working row + the script row per lane pair
+    k_fuzz_reset<1, false><<<n, 32, 2 * kRowWords * 4, S(stream)>>>(sp);
+  } else if ((int64_t)n <= (int64_t)sms * 64) {
+    // 8 episodes per warp, both states in shared rows (shared-space stores
+    // only), realize rows copied out coalesced (scripts/ab_env.sh: 1.5% on the
+    // 4096-env step, 4% on C3 over the streamed 4-episode form)
+    set_max_smem(k_fuzz_reset_sh<8>, 16 * kRowWords * 4);
+    k_fuzz_reset_sh<8><<<(n + 7) / 8, 32, 16 * kRowWords * 4, S(stream)>>>(sp);
+  } else {
+    // large batches (throughput): streamed seeding, one shared row per episode
+    set_max_smem(k_fuzz_reset<8, true>, 8 * kRowWords * 4);
+    k_fuzz_reset<8, true><<<(n + 7) / 8, 32, 8 * kRowWords * 4, S(stream)>>>(sp);
   }
 }
 

@@ -3,8 +3,8 @@
 
     compute-sanitizer --tool racecheck python tests/sanitize_cases.py [case ...]
 
-Cases: fuzz_ev (k_fuzz_reset + k_synth_cta with in-kernel event lists, both
-CTA shapes), fuzz (tl_fuzz), label (k_label vector + generic bodies, f32 and
+Cases: fuzz_ev (k_fuzz_reset + k_synth_warp + k_scan_emit, long and short
+episode configs), fuzz (tl_fuzz), label (k_label vector + generic bodies, f32 and
 f64, k_scan_emit), env (k_env_reset + k_env_step, both lane mappings),
 filter (k_filter_*), validate (k_validate), predicates, analytics.
 Each case checks its result against the oracle / its own invariants so a
