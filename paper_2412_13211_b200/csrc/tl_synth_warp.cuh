@@ -138,14 +138,16 @@ __device__ __forceinline__ int claim_episode_warp(const SynthParams& p, int endv
   return __ldcg(&p.order[(int64_t)(kLenBuckets - 1 - k) * p.n_env + (t - (k > 0 ? start : 0))]);
 }
 
-template <bool FUZZ, int DOFMAX, int NW>
-__global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
+// DOFX: the arm dof when fixed at compile time (7: every fuzz batch and the
+// usual realize batch -- the emission then has no dof branches), 0 = runtime
+template <bool FUZZ, int DOFMAX, int NW, int DOFX>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr uint32_t kMask = WarpCfg<DOFMAX>::kMask;
   constexpr int kSteps = WarpCfg<DOFMAX>::kSteps;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   WarpSmem<DOFMAX>& S = reinterpret_cast<WarpSmem<DOFMAX>*>(smem_raw)[warp];
-  const int dof = p.out.dof;
+  const int dof = DOFX ? DOFX : p.out.dof;
   float* __restrict__ P = reinterpret_cast<float*>(p.out.planes);
   const int64_t stride = p.out.plane_stride;
   const float fnan = __int_as_float(0x7fc00000);
@@ -354,62 +356,65 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
             break;
           }
         }
-        // ---- emit + write + indicator bits (cum patched below) -----------------
-        uint32_t ind = 0, errb = 0;
+        // ---- emit + write, and the cum chain, in one straight-line block -------
+        // Every lane runs the emission (invalid lanes' stores are predicated
+        // off) and the 32 chain steps are unconditional, so the compiler can
+        // interleave the serial f64 chain with the independent draws.
+        const int cnt = min(32, r_end - r0);
+        const int jx = exc_rec >= r0 ? min(cnt, exc_rec - r0) : 0;  // chain records [j0, jx)
+        const int64_t rr = rs + r;
+        const StepSt stv = S.st[sidx];
+        const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
+        float* __restrict__ dst = P + rr;
+        // at-rest records select 0.  The record's emit words are contiguous in
+        // the ring (apron), and rng.uniform(a, b) = a + (b - a) * (k * 2^-53)
+        // is evaluated as a + ((b - a) * 2^-53) * k: the same real product,
+        // so the same rounding, with the scaled span folded at compile time
+        const uint2* rw = ring2 + ((eo & kMask) >> 1);
+        TL_ASSERT(!(valid && emit) || (eo + 2u * (2 * dof + 5) <= produced &&
+                                       produced - eo <= (uint32_t)WarpCfg<DOFMAX>::kRing &&
+                                       (eo & kMask) + 2u * (2 * dof + 5) <=
+                                           (uint32_t)(WarpCfg<DOFMAX>::kRing + WarpCfg<DOFMAX>::kApron)));
+        auto draw = [&](const uint2* w, double a, double span) -> float {
+          const uint2 wv = *w;
+          const float v = __double2float_rn(uniform_k53(a, span * 0x1.0p-53, wv.x, wv.y));
+          return emit ? v : 0.f;
+        };
+        RecV<float> v;
+        float mq = 0.f, mqd = 0.f;
+#pragma unroll
+        for (int i = 0; i < DOFMAX; i++) {
+          if (i < dof) {
+            const float q = draw(rw + i, -0.3, 0.3 - -0.3);
+            if (valid) *dst = q;
+            dst += stride;
+            mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < DOFMAX; i++) {
+          if (i < dof) {
+            const float qd = draw(rw + dof + i, -0.4, 0.4 - -0.4);
+            if (valid) *dst = qd;
+            dst += stride;
+            mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
+          }
+        }
+        const uint2* r2 = rw + 2 * dof;
+        v.tor = draw(r2, -0.05, 0.05 - -0.05);
+        v.vx = draw(r2 + 1, -0.2, 0.2 - -0.2);
+        v.vy = draw(r2 + 2, -0.2, 0.2 - -0.2);
+        v.om = draw(r2 + 3, -0.3, 0.3 - -0.3);
+        v.der = draw(r2 + 4, 0.2, 1.0 - 0.2);
+        v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
+        v.force = stv.force;
+        v.cum = 0.f;  // over = false here; cum_patch_bits applies the real value
+        v.art = stv.art;
+        v.g = stv.grasped != 0;
+        v.qdm = mqd;
+        v.jm = mq;
+        v.jm_d = 0.0;
         if (valid) {
-          const int64_t rr = rs + r;
-          const StepSt stv = S.st[sidx];
-          const uint32_t eo = (uint32_t)(o + 2 * adv + 2 * app);
-          float* __restrict__ dst = P + rr;
-          // branch-free: every draw is computed, at-rest records select 0.
-          // The record's emit words are contiguous in the ring (apron), and
-          // rng.uniform(a, b) = a + (b - a) * (k * 2^-53) is evaluated as
-          // a + ((b - a) * 2^-53) * k: the same real product, so the same
-          // rounding, with the scaled span folded at compile time
-          const uint2* rw = ring2 + ((eo & kMask) >> 1);
-          TL_ASSERT(!emit || (eo + 2u * (2 * dof + 5) <= produced &&
-                              produced - eo <= (uint32_t)WarpCfg<DOFMAX>::kRing &&
-                              (eo & kMask) + 2u * (2 * dof + 5) <=
-                                  (uint32_t)(WarpCfg<DOFMAX>::kRing + WarpCfg<DOFMAX>::kApron)));
-          auto draw = [&](const uint2* w, double a, double span) -> float {
-            const uint2 wv = *w;
-            const float v = __double2float_rn(uniform_k53(a, span * 0x1.0p-53, wv.x, wv.y));
-            return emit ? v : 0.f;
-          };
-          RecV<float> v;
-          float mq = 0.f, mqd = 0.f;
-#pragma unroll
-          for (int i = 0; i < DOFMAX; i++) {
-            if (i < dof) {
-              const float q = draw(rw + i, -0.3, 0.3 - -0.3);
-              *dst = q;
-              dst += stride;
-              mq = i == 0 ? fabsf(q) : pymax_step(mq, fabsf(q));
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < DOFMAX; i++) {
-            if (i < dof) {
-              const float qd = draw(rw + dof + i, -0.4, 0.4 - -0.4);
-              *dst = qd;
-              dst += stride;
-              mqd = i == 0 ? fabsf(qd) : pymax_step(mqd, fabsf(qd));
-            }
-          }
-          const uint2* r2 = rw + 2 * dof;
-          v.tor = draw(r2, -0.05, 0.05 - -0.05);
-          v.vx = draw(r2 + 1, -0.2, 0.2 - -0.2);
-          v.vy = draw(r2 + 2, -0.2, 0.2 - -0.2);
-          v.om = draw(r2 + 3, -0.3, 0.3 - -0.3);
-          v.der = draw(r2 + 4, 0.2, 1.0 - 0.2);
-          v.dist = z.has_goal ? __double2float_rn(dist_rec) : fnan;
-          v.force = stv.force;
-          v.cum = 0.f;  // over = false here; cum_patch_bits applies the real value
-          v.art = stv.art;
-          v.g = stv.grasped != 0;
-          v.qdm = mqd;
-          v.jm = mq;
-          v.jm_d = 0.0;
           dst[0] = v.tor;
           dst[stride] = v.vx;
           dst[2 * stride] = v.vy;
@@ -419,35 +424,25 @@ __global__ void __launch_bounds__(NW * 32) k_synth_warp(SynthParams p) {
           dst[6 * stride] = v.force;
           dst[8 * stride] = v.art;
           p.out.grasped[rr] = (uint8_t)v.g;
-          record_bits(c, v, sc_ru, sc_d, ind, errb);
         }
-        // ---- cum_robot_force (synth.py:192-196, :210-213): serial f64, all
-        // lanes; lane j keeps record r0 + j.  Record 0 never draws; every
-        // later record draws until the ExcessiveCollisions record, which
-        // jumps to 1.05*limit for good.
-        const int cnt = min(32, r_end - r0);
-        const int jx = exc_rec >= r0 ? min(cnt, exc_rec - r0) : 0;  // draws in [j0, jx)
-        float my_cum = 0.f;
-        int j = 0;
-        if (r0 == 0) j = 1;  // record 0: cum 0
-        for (; j + 8 <= jx; j += 8) {
-          double rg[8];
+        // cum_robot_force (synth.py:192-196, :210-213), every lane, lane j
+        // keeps record r0 + j.  S.radv is 0.0 for records that do not advance
+        // (record 0, after ExcessiveCollisions, past the wave), and cum + 0.0
+        // == cum, so all 32 steps run unconditionally; the ExcessiveCollisions
+        // record and everything after it take 1.05*limit below.
+        double my_cum_d = 0.0;
 #pragma unroll
-          for (int k = 0; k < 8; k++) rg[k] = S.radv[j + k];
-#pragma unroll
-          for (int k = 0; k < 8; k++) {
-            cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), rg[k]));
-            if (lane == j + k) my_cum = __double2float_rn(cum);
-          }
-        }
-        for (; j < jx; j++) {
+        for (int j = 0; j < 32; j++) {
           cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), S.radv[j]));
-          if (lane == j) my_cum = __double2float_rn(cum);
+          my_cum_d = lane == j ? cum : my_cum_d;
         }
-        if (jx < cnt && r0 + cnt > exc_rec) {
+        if (jx < cnt) {  // the wave reaches the ExcessiveCollisions record (warp-uniform)
           cum = z.L105;
-          if (lane >= j) my_cum = __double2float_rn(cum);
+          if (lane >= max(jx, r0 == 0 ? 1 : 0)) my_cum_d = cum;
         }
+        const float my_cum = __double2float_rn(my_cum_d);
+        uint32_t ind = 0, errb = 0;
+        record_bits(c, v, sc_ru, sc_d, ind, errb);
         // ---- patch the cum bits, edges, label fold ------------------------------
         uint32_t indp = 0;
         if (valid) {

@@ -419,8 +419,12 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
     return check_launch();
   }
 #endif
-  const SynthWarpKernel k = fuzz ? (small ? k_synth_warp<true, 7, kSynthWarps> : k_synth_warp<true, 16, kSynthWarps>)
-                                 : (small ? k_synth_warp<false, 7, kSynthWarps> : k_synth_warp<false, 16, kSynthWarps>);
+  const bool d7 = sp.out.dof == 7;
+  const SynthWarpKernel k =
+      fuzz ? (d7 ? k_synth_warp<true, 7, kSynthWarps, 7>
+                 : small ? k_synth_warp<true, 7, kSynthWarps, 0> : k_synth_warp<true, 16, kSynthWarps, 0>)
+           : (d7 ? k_synth_warp<false, 7, kSynthWarps, 7>
+                 : small ? k_synth_warp<false, 7, kSynthWarps, 0> : k_synth_warp<false, 16, kSynthWarps, 0>);
   const int smem = kSynthWarps * (small ? (int)sizeof(WarpSmem<7>) : (int)sizeof(WarpSmem<16>));
   set_max_smem(k, smem);
   int per_sm = 0;
