@@ -60,8 +60,15 @@ __device__ __forceinline__ uint32_t mt_temper(uint32_t y) {
 }
 
 __device__ __forceinline__ uint32_t mt_mix(uint32_t a, uint32_t b, uint32_t src) {
-  uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
-  return src ^ (y >> 1) ^ ((0u - (y & 1u)) & 0x9908b0dfu);
+  // y = (a & UPPER) | (b & LOWER) in one LOP3 with a single mask constant;
+  // y & 1 == b & 1, so the MATRIX_A term is a predicate + SEL on b; then one
+  // three-way XOR: 5 ALU ops per word (the compiler's own form used 7)
+  uint32_t y, mag, r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(y) : "r"(a), "r"(b), "r"(0x80000000u));
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, 1;\n\tsetp.ne.b32 p, t, 0;\n\t"
+      "selp.b32 %0, 0x9908b0df, 0, p;\n\t}" : "=r"(mag) : "r"(b));
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(src), "r"(y >> 1), "r"(mag));
+  return r;
 }
 
 // random.Random(int) seeding of one state (one thread; init_by_array of
@@ -260,7 +267,10 @@ struct MtLane {
   uint32_t* mt;
   int idx;  // next word of the current block (0 right after seeding)
   int pre;  // words [0, pre) of the first block are already regenerated in place
-  const uint32_t* tw = nullptr;  // their tempered values (prepare_block_warp), or null
+  // their tempered values at mt[tw + i] (prepare_block_warp), tw = 0: none.
+  // An offset, not a pointer: a null test on a shared-memory pointer costs an
+  // S2R (shared window) per word in the serial sampler
+  int tw = 0;
   // regenerate words [0, n) (n <= 227: they read old words only) with
   // independent loads, so the serial sampler only tempers them
   __device__ __forceinline__ void prepare(int n) {
@@ -275,7 +285,7 @@ struct MtLane {
   }
   __device__ __forceinline__ uint32_t genrand() {
     if (idx < pre) {
-      const uint32_t x = tw ? tw[idx] : mt_temper(mt[idx]);
+      const uint32_t x = tw ? mt[tw + idx] : mt_temper(mt[idx]);
       idx++;
       return x;
     }
@@ -295,8 +305,10 @@ struct MtLane {
   // a warp in CPython's three dependency phases (0..226 read old words only,
   // 227..453 read new words 0..226, 454..623 read new 227..396 and word 0);
   // every lane of the warp calls it, then one lane samples with pre = 624;
-  // `tout` receives the tempered words (the serial sampler only loads them)
-  __device__ __forceinline__ void prepare_block_warp(uint32_t* tout) {
+  // mt[tw_off + i] receives the tempered words (the serial sampler only
+  // loads them), tw_off > 0
+  __device__ __forceinline__ void prepare_block_warp(int tw_off) {
+    uint32_t* tout = mt + tw_off;
     const int lane = lane_id();
     uint32_t v[8];
 #pragma unroll
@@ -337,7 +349,7 @@ struct MtLane {
     __syncwarp();
     idx = 0;
     pre = kMtN;
-    tw = tout;
+    tw = tw_off;
   }
   __device__ __forceinline__ double random() {
     uint32_t a = genrand() >> 5, b = genrand() >> 6;

@@ -143,6 +143,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
     const int32_t g = R.randint(1, cfg.max_gap);
     if (n < cap) { sk[n] = (uint8_t)ev; sg[n] = g; gaps += g; n++; } else overflow = true;
   };
+  if (threadIdx.x == 0) TL_STAMP(4);
   sc.tail = R.randint(1, cfg.max_tail);                                  // :372
   sc.initial_grasped = 0;
   sc.initial_contact = 0;
@@ -175,6 +176,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
   }
   bool contact_used = contact;                                           // :461
   const long n_target = (long)rint(__dmul_rn((double)R.randint(0, cfg.max_events), cfg.edge_density));
+  if (threadIdx.x == 0) TL_STAMP(5);
   for (long it = 0; it < n_target; it++) {                               // :464-474
     // the legal moves (at most 3), packed one byte each into a register
     // (no local-memory array): move i = (mv >> 8i) & 0xff
@@ -215,6 +217,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
       case TL_EV_OPEN: level = TL_LVL_OPEN; break;
     }
   }
+  if (threadIdx.x == 0) TL_STAMP(6);
   bool feasible;                                                         // :476-483
   if (kind == TL_PICK) feasible = grasped;
   else if (kind == TL_PLACE) feasible = !grasped && in_goal;
@@ -242,6 +245,7 @@ __device__ int sample_script(MtLane& R, int kind, const tl_fuzz_cfg& cfg,
   } else if (cfg.edge_density > 0 && R.random() < 0.15) {               // :504-505
     push(TL_EV_EXCESSIVE_COLLISIONS);
   }
+  if (threadIdx.x == 0) TL_STAMP(7);
   sc.n_steps = n;
   return overflow ? -1 : n;
 }
@@ -399,9 +403,12 @@ __device__ __forceinline__ StepSt make_st(const RzConst& z, const PlanSt& p, int
 }
 
 // random_script + the episode's script record, length bucket and record
-// layout (one thread; R = the freshly seeded script RNG)
-__device__ __forceinline__ void reset_script(const SynthParams& p, int64_t e, int64_t seed,
-                                             MtLane& R) {
+// layout (one thread; R = the freshly seeded script RNG).  Returns the
+// episode's length bucket; with place_order the thread also takes its slot
+// in the longest-first order by a global atomic (else the caller does,
+// aggregated per CTA).
+__device__ __forceinline__ int reset_script(const SynthParams& p, int64_t e, int64_t seed,
+                                            MtLane& R, bool place_order = true) {
   const int ms = p.cfg.max_events + 4;
   tl_script t;
   uint8_t* sk = p.step_kind + e * ms;
@@ -417,8 +424,9 @@ __device__ __forceinline__ void reset_script(const SynthParams& p, int64_t e, in
   t.seed = seed ^ 0x5EED;
   t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
   p.scripts[e] = t;
-  if (p.order) {  // length bucket for the realize kernel's longest-first claims
-    const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / 64);
+  // length bucket for the realize kernel's longest-first claims
+  const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / 64);
+  if (p.order && place_order) {
     const unsigned slot = atomicAdd(&p.tickets[kTkBucket + b], 1u);
     p.order[(int64_t)b * p.n_env + slot] = (int32_t)e;
   }
@@ -427,6 +435,7 @@ __device__ __forceinline__ void reset_script(const SynthParams& p, int64_t e, in
     p.out.rec_start[e] = e * p.cap_per_env;
     p.out.n_rec[e] = t.n_steps < 0 ? 0 : (int)nr;
   }
+  return b;
 }
 
 __device__ __forceinline__ void reset_counters(const SynthParams& p) {
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(E * 32) k_fuzz_reset_w(SynthParams p) {
   const int64_t e = e0 + warp;
   if (e >= p.n_env) return;
   MtLane R{rows + warp * kRowWords, 0, 0};
-  R.prepare_block_warp(rows + E * kRowWords + warp * kMtN);
+  R.prepare_block_warp((E - warp) * kRowWords + warp * kMtN);
   if (threadIdx.x == 0) TL_STAMP(2);
   if (lane == 0) reset_script(p, e, p.seeds[e], R);
   if (threadIdx.x == 0) TL_STAMP(3);
@@ -554,6 +563,66 @@ __global__ void __launch_bounds__(32) k_fuzz_reset_sh(SynthParams p) {
     reset_script(p, e, seed, R);
   }
   if (lane == 0) TL_STAMP(2);
+}
+
+// Mid-size batches: a CTA of E warps owns E episodes.  Warp 0 seeds all 2E
+// states into shared rows (lane 2j: script RNG of episode j, 2j+1: realize
+// RNG; shared-space stores only), the E warps copy the realize rows out
+// (coalesced) and regenerate their episode's first MT block (32 lanes,
+// tempered copy), then lane 0 of warp j samples random_script -- one sampler
+// per warp, no divergence between episodes.  The longest-first order slots
+// are taken per CTA: a shared histogram, then one global atomic per bucket.
+template <int E>
+__global__ void __launch_bounds__(E * 32) k_fuzz_reset_cta(SynthParams p) {
+  static_assert(E >= 1 && E <= 16, "2E seeding lanes in one warp");
+  // [2E][kRowWords]: the realize rows (odd) take the tempered words once copied out
+  extern __shared__ uint32_t rows[];
+  __shared__ int s_cnt[kLenBuckets], s_base[kLenBuckets];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  if (threadIdx.x < kLenBuckets) s_cnt[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.tickets) reset_counters(p);
+  if (threadIdx.x == 0) TL_STAMP(0);
+  if (warp == 0) {
+    const int j = lane >> 1;
+    const int64_t e = e0 + j;
+    if (j < E && e < p.n_env) {
+      const int64_t seed = p.seeds[e];
+      const int64_t sd = (lane & 1) ? (seed ^ 0x5EED) : seed;
+      const uint64_t n = sd < 0 ? (uint64_t)0 - (uint64_t)sd : (uint64_t)sd;
+      const uint32_t k0 = (uint32_t)n, k1 = (uint32_t)(n >> 32);
+      uint32_t* row = rows + lane * kRowWords;
+      if (k1) mt_seed_stream_impl<2>(k0, k1, row);
+      else mt_seed_stream_impl<1>(k0, 0u, row);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) TL_STAMP(1);
+  const int64_t e = e0 + warp;
+  int b = -1, rank = 0;
+  if (e < p.n_env) {
+    {  // the realize state of this warp's episode, out to global memory
+      const uint32_t* src = rows + (2 * warp + 1) * kRowWords;
+      uint32_t* dst = p.states + e * kMtN;
+#pragma unroll 4
+      for (int i = lane; i < kMtN; i += 32) dst[i] = src[i];
+    }
+    __syncwarp();  // the row is read out before it takes the tempered words
+    MtLane R{rows + 2 * warp * kRowWords, 0, 0};
+    R.prepare_block_warp(kRowWords);  // into the realize row that follows
+    if (threadIdx.x == 0) TL_STAMP(2);
+    if (lane == 0) {
+      b = reset_script(p, e, p.seeds[e], R, false);
+      if (p.order) rank = atomicAdd(&s_cnt[b], 1);
+    }
+  }
+  if (!p.order) return;
+  __syncthreads();
+  if (threadIdx.x < kLenBuckets && s_cnt[threadIdx.x])
+    s_base[threadIdx.x] = (int)atomicAdd(&p.tickets[kTkBucket + threadIdx.x], (unsigned)s_cnt[threadIdx.x]);
+  __syncthreads();
+  if (b >= 0) p.order[(int64_t)b * p.n_env + s_base[b] + rank] = (int32_t)e;
+  if (threadIdx.x == 0) TL_STAMP(3);
 }
 
 // realize path: seed the realize RNG of given scripts (one thread per state,

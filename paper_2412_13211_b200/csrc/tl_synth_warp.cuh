@@ -47,6 +47,7 @@ struct WarpSmem {
   StepSt st[kSteps + 1];
   double dist_after[kSteps];
   double radv[32];
+  double cumw[32];   // the wave's cum_robot_force values (chain step j -> lane j)
   uint8_t kind[kSteps];
   uint8_t sflag[kSteps];
   int32_t misc[16];
@@ -138,6 +139,18 @@ __device__ __forceinline__ int claim_episode_warp(const SynthParams& p, int endv
   return __ldcg(&p.order[(int64_t)(kLenBuckets - 1 - k) * p.n_env + (t - (k > 0 ? start : 0))]);
 }
 
+#ifdef TL_PHASES
+// per-warp timeline of the last launch (profiling build only,
+// scripts/warp_timeline.py): [w][0] start, [w][1] end (globaltimer ns),
+// [w][2] records realized, [w][3] episodes
+__device__ unsigned long long g_tl_warp[4096][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // DOFX: the arm dof when fixed at compile time (7: every fuzz batch and the
 // usual realize batch -- the emission then has no dof branches), 0 = runtime
 template <bool FUZZ, int DOFMAX, int NW, int DOFX>
@@ -153,6 +166,11 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
   const float fnan = __int_as_float(0x7fc00000);
   const uint2* ring2 = reinterpret_cast<const uint2*>(S.wb);
   const int endv = p.order ? bucket_end_lane(p) : 0;
+#ifdef TL_PHASES
+  const int gw = blockIdx.x * NW + warp;
+  unsigned long long w_recs = 0, w_eps = 0;
+  if (lane == 0 && gw < 4096) g_tl_warp[gw][0] = gtimer();
+#endif
 
   for (int e = claim_episode_warp(p, endv); e < p.n_env; e = claim_episode_warp(p, endv)) {
     // ---------------- script + seeded RNG state -------------------------------
@@ -430,12 +448,15 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
         // (record 0, after ExcessiveCollisions, past the wave), and cum + 0.0
         // == cum, so all 32 steps run unconditionally; the ExcessiveCollisions
         // record and everything after it take 1.05*limit below.
-        double my_cum_d = 0.0;
+        // each step's value goes to S.cumw[j] (one broadcast store per step),
+        // read back by lane j after the chain
 #pragma unroll
         for (int j = 0; j < 32; j++) {
           cum = __dadd_rn(cum, __dmul_rn(__dmul_rn(__dsub_rn(z.L09, cum), 0.05), S.radv[j]));
-          my_cum_d = lane == j ? cum : my_cum_d;
+          S.cumw[j] = cum;
         }
+        __syncwarp();
+        double my_cum_d = S.cumw[lane];  // record 0: radv 0, cum 0
         if (jx < cnt) {  // the wave reaches the ExcessiveCollisions record (warp-uniform)
           cum = z.L105;
           if (lane >= max(jx, r0 == 0 ? 1 : 0)) my_cum_d = cum;
@@ -478,7 +499,18 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
       const tl_label L = make_label(c, LS, d0, p.rules);
       if (lane == 0) p.labels[e] = L;
     }
+#ifdef TL_PHASES
+    w_recs += n_rec;
+    w_eps++;
+#endif
   }
+#ifdef TL_PHASES
+  if (lane == 0 && gw < 4096) {
+    g_tl_warp[gw][1] = gtimer();
+    g_tl_warp[gw][2] = w_recs;
+    g_tl_warp[gw][3] = w_eps;
+  }
+#endif
   if (p.order) {  // the last CTA out leaves the length buckets at zero for the next launch
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -336,6 +336,19 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
     k_fuzz_reset_w<16><<<(n + 15) / 16, 16 * 32, 16 * (kRowWords + kMtN) * 4, S(stream)>>>(sp);
     return;
   }
+  if (const char* fc = ab_env("TL_RESET_CTA")) {
+    const int e = atoi(fc);
+    if (e == 16) {
+      const int smem = 16 * 2 * kRowWords * 4;
+      set_max_smem(k_fuzz_reset_cta<16>, smem);
+      k_fuzz_reset_cta<16><<<(n + 15) / 16, 16 * 32, smem, S(stream)>>>(sp);
+    } else {
+      const int smem = 8 * 2 * kRowWords * 4;
+      set_max_smem(k_fuzz_reset_cta<8>, smem);
+      k_fuzz_reset_cta<8><<<(n + 7) / 8, 8 * 32, smem, S(stream)>>>(sp);
+    }
+    return;
+  }
   if (ab_env("TL_RESET_SH")) {
     const int e = atoi(ab_env("TL_RESET_SH"));
     const int smem = 2 * e * kRowWords * 4;
@@ -363,16 +376,14 @@ static void launch_fuzz_reset(SynthParams& sp, void* stream) {
     return;
   }
 #endif
-  if ((int64_t)n <= (int64_t)sms * 8) {
-    // one episode per warp: the sampler is serial branchy code that diverges
-    // across episodes; one working row + the script row per lane pair
-    k_fuzz_reset<1, false><<<n, 32, 2 * kRowWords * 4, S(stream)>>>(sp);
-  } else if ((int64_t)n <= (int64_t)sms * 64) {
-    // 8 episodes per warp, both states in shared rows (shared-space stores
-    // only), realize rows copied out coalesced (scripts/ab_env.sh: 1.5% on the
-    // 4096-env step, 4% on C3 over the streamed 4-episode form)
-    set_max_smem(k_fuzz_reset_sh<8>, 16 * kRowWords * 4);
-    k_fuzz_reset_sh<8><<<(n + 7) / 8, 32, 16 * kRowWords * 4, S(stream)>>>(sp);
+  if ((int64_t)n <= (int64_t)sms * 64) {
+    // a CTA of 8 warps per 8 episodes: warp 0 seeds the 16 states into shared
+    // rows, one random_script sampler per warp, longest-first slots per CTA
+    // (scripts/ab_env.sh: -2.3% on the 4096-env step, -4.5% at 1024, -2.8% C3
+    // against the lane-per-sampler forms)
+    const int smem = 8 * 2 * kRowWords * 4;
+    set_max_smem(k_fuzz_reset_cta<8>, smem);
+    k_fuzz_reset_cta<8><<<(n + 7) / 8, 8 * 32, smem, S(stream)>>>(sp);
   } else {
     // large batches (throughput): streamed seeding, one shared row per episode
     set_max_smem(k_fuzz_reset<8, true>, 8 * kRowWords * 4);
@@ -861,6 +872,11 @@ int tl_compact_records(const tl_records* src, int32_t n_env, const int64_t* dst_
 }
 
 #ifdef TL_PHASES
+extern "C" int tl_warp_timeline(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tl_warp, sizeof(g_tl_warp)) == cudaSuccess ? TL_OK : TL_E_CUDA;
+}
+#endif
+#if defined(TL_PHASES) && defined(TL_AB)
 extern "C" int tl_phase_read(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_tl_phase, sizeof(unsigned long long) * 16) != cudaSuccess) return TL_E_CUDA;
   if (reset) {

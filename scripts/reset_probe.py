@@ -28,3 +28,6 @@ buf = np.zeros(128, np.uint64)
 lib.tl_prof_read(buf.ctypes.data)
 t = buf.astype(np.int64)
 print(f"n={n} reset block 0: seed {t[1]-t[0]}  prepare {t[2]-t[1]}  sample {t[3]-t[2]}  total {t[3]-t[0]} cycles")
+if t[4] and t[7] > t[4]:
+    print(f"  sampler (thread 0): head {t[5]-t[4]}  event loop {t[6]-t[5]}  suffix {t[7]-t[6]}  "
+          f"after sampling {t[3]-t[7]} cycles")
