@@ -255,10 +255,11 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask,
             tl_script* scripts, uint8_t* step_mask, tl_label* labels,
             void* scratch, void* stream);
 
-/* tl_fuzz + the ordered event lists in the same launch pair: ev_off[n+1],
- * (ev_kind, ev_t) at ev_off[e] as tl_scan_emit_events would produce them
- * (a decoupled look-back over episodes inside the realize kernel).
- * step_mask is required; ev_capacity >= 4 * n_env * cap_per_env. */
+/* tl_fuzz + the ordered event lists: ev_off[n+1], (ev_kind, ev_t) at
+ * ev_off[e] exactly as tl_scan_emit_events produces them (the reset, realize
+ * and k_scan_emit kernels back to back on `stream`; the outputs may be
+ * pinned host memory).  step_mask is required;
+ * ev_capacity >= 4 * n_env * cap_per_env. */
 int tl_fuzz_ev(const int64_t* seeds, int32_t n_env, int32_t subtask,
                const tl_fuzz_cfg* cfg /* host */,
                const tl_thresholds* th_realize /* host */,

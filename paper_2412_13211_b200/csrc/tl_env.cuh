@@ -401,13 +401,17 @@ __device__ __forceinline__ void env_stage_async_q(const uint32_t* __restrict__ m
   cp_async_commit();
 }
 
-template <int DOFMAX, int LPE>
+// STAGED: the 12 label csets are staged into shared memory once per block
+// (multi-step launches); single-step launches read the env's cset through L1
+// at use instead -- the staging round trip and block barrier were ~0.8 us of
+// a ~5.6 us single-step launch (scripts/ab_env_api.sh)
+template <int DOFMAX, int LPE, bool STAGED>
 __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
   using SM = EnvQSmem<DOFMAX, LPE>;
   constexpr int kQuad = LPE;  // lanes per env (4 or 8)
   extern __shared__ __align__(16) unsigned char env_smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(env_smem_raw);
-  {
+  if (STAGED) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(p.hdr->cs);
     uint32_t* d = reinterpret_cast<uint32_t*>(sm.cs);
     for (int i = threadIdx.x; i < (int)(sizeof(sm.cs) / 4); i += blockDim.x) d[i] = __ldg(src + i);
@@ -429,7 +433,8 @@ __global__ void __launch_bounds__(kEnvQThreads) k_env_step(EnvParams p) {
   }
   RzConst z;
   env_rz(z, s, p.hdr->th, p.dof);
-  const tl_cset& c = sm.cs[s.subtask * 3 + s.art_kind];
+  const tl_cset& c = STAGED ? sm.cs[s.subtask * 3 + s.art_kind]
+                            : p.hdr->cs[s.subtask * 3 + s.art_kind];  // L1-cached reads at use
   uint32_t* mt = p.mt + (size_t)e * kMtN;
   uint32_t* row = sm.buf + le * SM::kStride;
   const int dof = z.dof, ne = z.ne;

@@ -689,12 +689,23 @@ int tl_env_step(void* state, int32_t n_env, int32_t dof, const uint8_t* actions,
     const int per_block = kEnvQThreads / lpe;
     kern<<<(n_env + per_block - 1) / per_block, kEnvQThreads, smem, S(stream)>>>(ep);
   };
+  const bool staged = k_steps > 1;
   if (dof <= 7) {
-    if (wide) go(k_env_step<7, 8>, 8, sizeof(EnvQSmem<7, 8>));
-    else go(k_env_step<7, 4>, 4, sizeof(EnvQSmem<7, 4>));
+    if (wide) {
+      if (staged) go(k_env_step<7, 8, true>, 8, sizeof(EnvQSmem<7, 8>));
+      else go(k_env_step<7, 8, false>, 8, sizeof(EnvQSmem<7, 8>));
+    } else {
+      if (staged) go(k_env_step<7, 4, true>, 4, sizeof(EnvQSmem<7, 4>));
+      else go(k_env_step<7, 4, false>, 4, sizeof(EnvQSmem<7, 4>));
+    }
   } else {
-    if (wide) go(k_env_step<16, 8>, 8, sizeof(EnvQSmem<16, 8>));
-    else go(k_env_step<16, 4>, 4, sizeof(EnvQSmem<16, 4>));
+    if (wide) {
+      if (staged) go(k_env_step<16, 8, true>, 8, sizeof(EnvQSmem<16, 8>));
+      else go(k_env_step<16, 8, false>, 8, sizeof(EnvQSmem<16, 8>));
+    } else {
+      if (staged) go(k_env_step<16, 4, true>, 4, sizeof(EnvQSmem<16, 4>));
+      else go(k_env_step<16, 4, false>, 4, sizeof(EnvQSmem<16, 4>));
+    }
   }
   return check_launch();
 }
