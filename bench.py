@@ -824,7 +824,7 @@ def main(argv=None):
                                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
                     "hist")
 
-    launches_per_step = 2 + (1 if world > 1 else 0)  # reset, realize(+events) [, histogram]
+    launches_per_step = 3 + (1 if world > 1 else 0)  # reset, realize, event lists [, histogram]
     for k in range(W):
         seeds_buf.copy_(all_seeds[K + k])
         graph.replay()
@@ -990,6 +990,9 @@ def main(argv=None):
             "issue_active": prof.get("issue_active"), "warps_active": prof.get("warps_active"),
             "traffic": prof.get("dram_bytes_per_launch"),
             "profile": "profiles/r2_ncu_headline.json" if prof else None,
+            "realize_kernel": prof.get("realize_kernel"),
+            "note": ("floor = one episode's serial chains; the batch is also issue-bound: the "
+                     "realize kernel's issue_active (ncu, same config) says how full the SMs are"),
             "hbm": {"achieved": alg_bytes / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": alg_bytes / step_s / 1e9 / hbm_peak, "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": alg_bytes,

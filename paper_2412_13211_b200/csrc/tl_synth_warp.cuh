@@ -144,11 +144,20 @@ __device__ __forceinline__ int claim_episode_warp(const SynthParams& p, int endv
 // scripts/warp_timeline.py): [w][0] start, [w][1] end (globaltimer ns),
 // [w][2] records realized, [w][3] episodes
 __device__ unsigned long long g_tl_warp[4096][4];
+__device__ unsigned long long g_tl_wphase[16];  // clock64 deltas summed over warps, [15] waves
+#define TL_WPH(k)                                                                   \
+  do {                                                                              \
+    const long long _t = clock64();                                                 \
+    if (lane == 0) atomicAdd(&g_tl_wphase[(k)], (unsigned long long)(_t - ph_t));   \
+    ph_t = _t;                                                                      \
+  } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#else
+#define TL_WPH(k) do { } while (0)
 #endif
 
 // DOFX: the arm dof when fixed at compile time (7: every fuzz batch and the
@@ -170,6 +179,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
   const int gw = blockIdx.x * NW + warp;
   unsigned long long w_recs = 0, w_eps = 0;
   if (lane == 0 && gw < 4096) g_tl_warp[gw][0] = gtimer();
+  long long ph_t = clock64();
 #endif
 
   for (int e = claim_episode_warp(p, endv); e < p.n_env; e = claim_episode_warp(p, endv)) {
@@ -205,6 +215,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
 #pragma unroll
       for (int i = lane; i < kMtN / 4; i += 32) reinterpret_cast<uint4*>(S.mt)[i] = __ldcg(src + i);
     }
+    TL_WPH(9);  // 9: claim + script/state loads
     const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
     stage_cset(&S.cs, &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
     RzConst z;
@@ -213,6 +224,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
       fail(st0, -1);
       continue;
     }
+    TL_WPH(6);  // 6: cset staging + realizer init
     PlanSt ps;  // initial realizer state (synth.py:111-158)
     ps.force = (z.has_force && sc.initial_contact) ? 1.2 : 0.0;
     ps.grasped = sc.initial_grasped ? 1 : 0;
@@ -293,6 +305,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
         reinterpret_cast<double*>(&S.misc[10])[0] = q.art;
       }
       __syncwarp();
+      TL_WPH(7);  // 7: window load + plan
       const int perr = S.misc[0], pstep = S.misc[1];
       const int exc_rec = S.misc[14];
       const int r_begin = first_window ? 0 : tau_prev + 1;
@@ -328,6 +341,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
           }
         }
         seg_hint = __shfl_sync(kFull, s, 0);  // lane 0 holds the wave's first record
+        TL_WPH(1);  // 1: descriptors
         TL_ASSERT(!valid || (r < n_rec && s <= ns && sidx <= ns));
         const int need = valid ? o + 2 * adv + 2 * app + (emit ? 2 * z.ne : 0) : 0;
         const int need_max = __reduce_max_sync(kFull, need);
@@ -335,6 +349,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
           twist_block_warp<DOFMAX>(S.mt, S.wb, produced);
           produced += kMtN;
         }
+        TL_WPH(2);  // 2: twist
         auto rnd = [&](int woff) {
           const uint2 wv = ring2[((uint32_t)woff & kMask) >> 1];
           return rand53(wv.x, wv.y);
@@ -374,6 +389,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
             break;
           }
         }
+        TL_WPH(3);  // 3: draws before emission + error check (+ the twist: phase 2)
         // ---- emit + write, and the cum chain, in one straight-line block -------
         // Every lane runs the emission (invalid lanes' stores are predicated
         // off) and the 32 chain steps are unconditional, so the compiler can
@@ -464,6 +480,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
         const float my_cum = __double2float_rn(my_cum_d);
         uint32_t ind = 0, errb = 0;
         record_bits(c, v, sc_ru, sc_d, ind, errb);
+        TL_WPH(4);  // 4: emission || chain
         // ---- patch the cum bits, edges, label fold ------------------------------
         uint32_t indp = 0;
         if (valid) {
@@ -477,6 +494,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
         ind_carry = __shfl_sync(kFull, indp, cnt - 1);
         lstate_fold(LS, mask, valid ? errb : 0u);
         __syncwarp();  // S.radv / S.dist_after are rewritten by the next wave
+        TL_WPH(5);  // 5: patch + fold
+#ifdef TL_PHASES
+        if (lane == 0) atomicAdd(&g_tl_wphase[15], 1ull);
+#endif
       }
       if (!err_code && perr) { err_code = perr; err_step = s_base + pstep; }
       if (err_code || last_window) break;
@@ -493,6 +514,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
       first_window = false;
       __syncwarp();  // the plan arrays are rewritten by the next window
     }
+    TL_WPH(10);  // 10: window tails
     if (err_code) {
       fail(err_code, err_step);
     } else {
@@ -503,6 +525,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
     w_recs += n_rec;
     w_eps++;
 #endif
+    TL_WPH(8);  // 8: label
   }
 #ifdef TL_PHASES
   if (lane == 0 && gw < 4096) {

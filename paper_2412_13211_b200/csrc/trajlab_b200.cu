@@ -886,6 +886,14 @@ int tl_compact_records(const tl_records* src, int32_t n_env, const int64_t* dst_
 extern "C" int tl_warp_timeline(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tl_warp, sizeof(g_tl_warp)) == cudaSuccess ? TL_OK : TL_E_CUDA;
 }
+extern "C" int tl_warp_phases(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_tl_wphase, sizeof(g_tl_wphase)) != cudaSuccess) return TL_E_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_tl_wphase, z, sizeof(z));
+  }
+  return TL_OK;
+}
 #endif
 #if defined(TL_PHASES) && defined(TL_AB)
 extern "C" int tl_phase_read(unsigned long long* out, int reset) {
