@@ -351,6 +351,31 @@ struct MtLane {
     pre = kMtN;
     tw = tw_off;
   }
+  // the first n <= 227 words only (they read old words), by the 32 lanes of a
+  // warp, tempered copies at mt[tw_off + i]; the lone sampler continues
+  // lazily from word n (the words it usually needs are all in the prefix)
+  template <int N>
+  __device__ __forceinline__ void prepare_prefix_warp(int tw_off) {
+    static_assert(N % 32 == 0 && N <= kMtN - kMtM, "prefix of old-only words");
+    const int lane = lane_id();
+    uint32_t v[N / 32];
+#pragma unroll
+    for (int k = 0; k < N / 32; k++) {
+      const int i = lane + 32 * k;
+      v[k] = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < N / 32; k++) {
+      const int i = lane + 32 * k;
+      mt[i] = v[k];
+      mt[tw_off + i] = mt_temper(v[k]);
+    }
+    __syncwarp();
+    idx = 0;
+    pre = N;
+    tw = tw_off;
+  }
   __device__ __forceinline__ double random() {
     uint32_t a = genrand() >> 5, b = genrand() >> 6;
     return __ull2double_rn(((uint64_t)a << 26) | b) * 0x1.0p-53;

@@ -75,7 +75,13 @@ struct SynthParams {
   int32_t* order;
 };
 
-constexpr int kLenBuckets = 16;
+#ifdef TL_BUCKET32
+constexpr int kLenBuckets = 32;   // longest-first buckets of 32 records
+constexpr int kBucketRecs = 32;
+#else
+constexpr int kLenBuckets = 16;   // longest-first buckets of 64 records
+constexpr int kBucketRecs = 64;
+#endif
 constexpr int kTkBucket = 4;  // tickets[kTkBucket + b]
 
 // ticket -> episode: tickets walk the length buckets from the longest down
@@ -425,7 +431,7 @@ __device__ __forceinline__ int reset_script(const SynthParams& p, int64_t e, int
   t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
   p.scripts[e] = t;
   // length bucket for the realize kernel's longest-first claims
-  const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / 64);
+  const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / kBucketRecs);
   if (p.order && place_order) {
     const unsigned slot = atomicAdd(&p.tickets[kTkBucket + b], 1u);
     p.order[(int64_t)b * p.n_env + slot] = (int32_t)e;
@@ -570,17 +576,14 @@ __global__ void __launch_bounds__(32) k_fuzz_reset_sh(SynthParams p) {
 // RNG; shared-space stores only), the E warps copy the realize rows out
 // (coalesced) and regenerate their episode's first MT block (32 lanes,
 // tempered copy), then lane 0 of warp j samples random_script -- one sampler
-// per warp, no divergence between episodes.  The longest-first order slots
-// are taken per CTA: a shared histogram, then one global atomic per bucket.
+// per warp, no divergence between episodes -- and takes its longest-first slot.
 template <int E>
 __global__ void __launch_bounds__(E * 32) k_fuzz_reset_cta(SynthParams p) {
   static_assert(E >= 1 && E <= 16, "2E seeding lanes in one warp");
   // [2E][kRowWords]: the realize rows (odd) take the tempered words once copied out
   extern __shared__ uint32_t rows[];
-  __shared__ int s_cnt[kLenBuckets], s_base[kLenBuckets];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t e0 = (int64_t)blockIdx.x * E;
-  if (threadIdx.x < kLenBuckets) s_cnt[threadIdx.x] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.tickets) reset_counters(p);
   if (threadIdx.x == 0) TL_STAMP(0);
   if (warp == 0) {
@@ -599,7 +602,6 @@ __global__ void __launch_bounds__(E * 32) k_fuzz_reset_cta(SynthParams p) {
   __syncthreads();
   if (threadIdx.x == 0) TL_STAMP(1);
   const int64_t e = e0 + warp;
-  int b = -1, rank = 0;
   if (e < p.n_env) {
     {  // the realize state of this warp's episode, out to global memory
       const uint32_t* src = rows + (2 * warp + 1) * kRowWords;
@@ -609,19 +611,13 @@ __global__ void __launch_bounds__(E * 32) k_fuzz_reset_cta(SynthParams p) {
     }
     __syncwarp();  // the row is read out before it takes the tempered words
     MtLane R{rows + 2 * warp * kRowWords, 0, 0};
-    R.prepare_block_warp(kRowWords);  // into the realize row that follows
+    // the sampler reads ~40 words: regenerate the first 128 with 32 lanes,
+    // the rest lazily (a full-block prepare and a CTA-wide order aggregation
+    // measured 9k cycles slower per CTA, scripts/reset_probe_env.sh)
+    R.prepare_prefix_warp<128>(kRowWords);  // tempered copies into the realize row
     if (threadIdx.x == 0) TL_STAMP(2);
-    if (lane == 0) {
-      b = reset_script(p, e, p.seeds[e], R, false);
-      if (p.order) rank = atomicAdd(&s_cnt[b], 1);
-    }
+    if (lane == 0) reset_script(p, e, p.seeds[e], R, true);  // its own longest-first slot
   }
-  if (!p.order) return;
-  __syncthreads();
-  if (threadIdx.x < kLenBuckets && s_cnt[threadIdx.x])
-    s_base[threadIdx.x] = (int)atomicAdd(&p.tickets[kTkBucket + threadIdx.x], (unsigned)s_cnt[threadIdx.x]);
-  __syncthreads();
-  if (b >= 0) p.order[(int64_t)b * p.n_env + s_base[b] + rank] = (int32_t)e;
   if (threadIdx.x == 0) TL_STAMP(3);
 }
 
