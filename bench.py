@@ -557,11 +557,14 @@ def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
             "parity": "tests/test_gpu_shipped.py::test_c5_bench_scale_filter_vs_oracle"}
 
 
-def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None):
+def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None):
     """One fused fuzz step (tl_fuzz_ev: reset + realize + labels + ordered
     event lists) on preallocated buffers, captured as a CUDA graph.  host_out
     (pinned host tensors ev_off / ev_kind / ev_t, optionally labels): the
     kernel writes those outputs straight into host memory (zero-copy).
+    io (pinned host tensors seeds [n] int64, labels [n, 24] u8): the graph
+    also copies the seeds in (H2D) and the labels out (D2H), so one graph
+    launch is the whole host-to-host step.
     Returns (graph, seeds_buf, workspace, device event buffers)."""
     import ctypes
     import torch
@@ -587,12 +590,16 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None):
     rb_c = ws.records().c()
 
     def body(s):
+        if io is not None:
+            seeds_buf.copy_(io["seeds"], non_blocking=True)
         L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), n_env, kind, ctypes.byref(cfg_c),
                                ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
                                None, None, None, L.ptr(ws.step_mask), L.ptr(out["labels"]),
                                L.ptr(out["ev_off"]), L.ptr(out["ev_kind"]), L.ptr(out["ev_t"]),
                                ev_cap, L.ptr(ws.scratch), ctypes.c_void_p(s.cuda_stream)),
                 "tl_fuzz_ev")
+        if io is not None:
+            io["labels"].copy_(out["labels"], non_blocking=True)
     body(stream)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -809,6 +816,13 @@ def main(argv=None):
                    ev_t=torch.empty(ev_cap, dtype=torch.int32).pin_memory())
     graph, seeds_buf, ws, ev_dev = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg)
     graph_h, seeds_h, ws_h, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg, host_out=ev_host)
+    # 1 GPU: the whole host-to-host step as one graph (H2D seeds, tl_fuzz_ev
+    # with event lists into pinned host memory, D2H labels)
+    io = None
+    if world == 1:
+        io = dict(seeds=torch.empty(N_ENV, dtype=torch.int64).pin_memory(),
+                  labels=torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory())
+        graph_io, _, ws_io, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg, host_out=ev_host, io=io)
     hist = torch.zeros(L.N_MODES, dtype=torch.int64, device=dev)
     gathered = torch.empty((world * N_ENV, 24), dtype=torch.uint8, device=dev)
     # inputs resident in HBM: seeds of every step, rank-disjoint ranges
@@ -890,6 +904,17 @@ def main(argv=None):
             for k in range(K2):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
+                if io is not None and not with_records:
+                    io["seeds"].copy_(host_seeds[k])      # this step's inputs, pinned staging
+                    graph_io.replay()                     # H2D seeds, fuzz_ev, D2H labels
+                    stream.synchronize()
+                    wall += time.perf_counter() - t0
+                    NE = int(ev_host["ev_off"][N_ENV])
+                    recs += int(nrec_log[k].sum())
+                    h2d = N_ENV * 8
+                    d2h = max(d2h, N_ENV * 24 + (N_ENV + 1) * 8 + NE * 5)
+                    flush.zero_()
+                    continue
                 seeds_h.copy_(host_seeds[k], non_blocking=True)
                 graph_h.replay()                          # event lists -> pinned host
                 exchange(ws_h.labels)
@@ -925,7 +950,9 @@ def main(argv=None):
             return wall, recs, h2d, d2h
 
         t_e2e, e2e_recs, h2d_b, d2h_b = e2e_loop(False)
-        check = self_check(ws_h, ev_host, host_seeds[K2 - 1].numpy())
+        check = self_check(ws_io if io is not None else ws_h, ev_host, host_seeds[K2 - 1].numpy())
+        if io is not None and not torch.equal(io["labels"], ws_io.labels.cpu()):
+            raise RuntimeError("bench self-check: the D2H label copy differs from the device labels")
         t_e2r, e2r_recs, _, d2h_rb = e2e_loop(True)
         extras = {}
         if not args.no_extras:
@@ -1002,9 +1029,10 @@ def main(argv=None):
                 "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": K2,
                 "timing": "time.perf_counter around the calls + stream synchronize, per step, "
                           "max over ranks",
-                "note": "C-ABI tl_fuzz_ev with host buffers: pinned host seeds -> GPU (H2D), "
-                        "ordered event lists written by the kernel into pinned host memory "
-                        "(zero-copy), labels D2H (N>1: after the NCCL all-gather; histogram D2H)",
+                "note": "C-ABI tl_fuzz_ev with host buffers: the step's seeds into a pinned staging "
+                        "block (host copy), then one CUDA graph = H2D seeds + tl_fuzz_ev (ordered "
+                        "event lists written by k_scan_emit into pinned host memory, zero-copy) + "
+                        "D2H labels (N>1: separate copies around the NCCL all-gather; histogram D2H)",
                 "with_records": {"value": e2r_recs_all / t_e2r, "unit": "env-steps/s",
                                  "d2h_bytes_per_step": d2h_rb,
                                  "note": "same, plus tl_scan_counts + tl_compact_records into one "

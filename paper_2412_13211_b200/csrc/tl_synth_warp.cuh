@@ -209,22 +209,34 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
     const int n_rec = p.out.n_rec[e];
     TL_ASSERT(rs >= 0 && n_rec >= 0 && rs + n_rec <= p.out.plane_stride);
     TL_ASSERT(!FUZZ || n_rec <= p.cap_per_env);
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(p.states + (int64_t)e * kMtN);
-      __syncwarp();  // the previous episode is done with S.mt
-#pragma unroll
-      for (int i = lane; i < kMtN / 4; i += 32) reinterpret_cast<uint4*>(S.mt)[i] = __ldcg(src + i);
-    }
-    TL_WPH(9);  // 9: claim + script/state loads
+    // every load that only needs the script goes out together (one L2 round
+    // trip instead of three): the MT state and the cset by cp.async, the
+    // first window's step kinds and gaps into lane registers
     const int art_idx = (sc.subtask == TL_OPEN || sc.subtask == TL_CLOSE) ? sc.art_kind : 0;
-    stage_cset(&S.cs, &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
+    const int ns0 = min(sc.n_steps, kSteps);
+    const int kind0 = lane < ns0 ? (int)p.step_kind[sc.step_off + lane] : 0;
+    const int gap0 = lane < ns0 ? p.step_gap[sc.step_off + lane] : 0;
+    {
+      __syncwarp();  // the previous episode is done with S.mt and S.cs
+      const uint32_t* src = p.states + (int64_t)e * kMtN;
+#pragma unroll
+      for (int i = lane; i < kMtN / 4; i += 32) cp_async16(S.mt + 4 * i, src + 4 * i);
+      const uint32_t* cs = reinterpret_cast<const uint32_t*>(
+          &p.label_csets[sc.subtask * 3 + (art_idx < 0 || art_idx > 2 ? 0 : art_idx)]);
+      for (int i = lane; i < (int)(sizeof(tl_cset) / 4); i += 32)
+        cp_async4(reinterpret_cast<uint32_t*>(&S.cs) + i, cs + i);
+      cp_async_commit();
+    }
+    TL_WPH(9);  // 9: claim + script loads
     RzConst z;
     const int st0 = realizer_init(z, sc, p.th, dof);
+    cp_async_wait<0>();
+    __syncwarp();
     if (st0 != TL_OK) {
       fail(st0, -1);
       continue;
     }
-    TL_WPH(6);  // 6: cset staging + realizer init
+    TL_WPH(6);  // 6: state + cset arrival, realizer init
     PlanSt ps;  // initial realizer state (synth.py:111-158)
     ps.force = (z.has_force && sc.initial_contact) ? 1.2 : 0.0;
     ps.grasped = sc.initial_grasped ? 1 : 0;
@@ -263,9 +275,16 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
     for (;;) {
       const int ns = min(n_steps - s_base, kSteps);
       const bool last_window = s_base + ns >= n_steps;
-      for (int i = lane; i < ns; i += 32) {
-        S.kind[i] = p.step_kind[sc.step_off + s_base + i];
-        S.gap[i] = p.step_gap[sc.step_off + s_base + i];
+      if (first_window) {  // prefetched with the state
+        if (lane < ns) {
+          S.kind[lane] = (uint8_t)kind0;
+          S.gap[lane] = gap0;
+        }
+      } else {
+        for (int i = lane; i < ns; i += 32) {
+          S.kind[i] = p.step_kind[sc.step_off + s_base + i];
+          S.gap[i] = p.step_gap[sc.step_off + s_base + i];
+        }
       }
       __syncwarp();
       if (lane == 0) {  // plan: record/word layout + deterministic state
