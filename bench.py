@@ -816,13 +816,9 @@ def main(argv=None):
                    ev_t=torch.empty(ev_cap, dtype=torch.int32).pin_memory())
     graph, seeds_buf, ws, ev_dev = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg)
     graph_h, seeds_h, ws_h, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg, host_out=ev_host)
-    # 1 GPU: the whole host-to-host step as one graph (H2D seeds, tl_fuzz_ev
-    # with event lists into pinned host memory, D2H labels)
+    # (capturing the H2D / D2H copies into the step graph measured 3-5% slower
+    # end to end than separate async copies: scripts/e2e_variants.py)
     io = None
-    if world == 1:
-        io = dict(seeds=torch.empty(N_ENV, dtype=torch.int64).pin_memory(),
-                  labels=torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory())
-        graph_io, _, ws_io, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg, host_out=ev_host, io=io)
     hist = torch.zeros(L.N_MODES, dtype=torch.int64, device=dev)
     gathered = torch.empty((world * N_ENV, 24), dtype=torch.uint8, device=dev)
     # inputs resident in HBM: seeds of every step, rank-disjoint ranges
@@ -1029,10 +1025,9 @@ def main(argv=None):
                 "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": K2,
                 "timing": "time.perf_counter around the calls + stream synchronize, per step, "
                           "max over ranks",
-                "note": "C-ABI tl_fuzz_ev with host buffers: the step's seeds into a pinned staging "
-                        "block (host copy), then one CUDA graph = H2D seeds + tl_fuzz_ev (ordered "
-                        "event lists written by k_scan_emit into pinned host memory, zero-copy) + "
-                        "D2H labels (N>1: separate copies around the NCCL all-gather; histogram D2H)",
+                "note": "C-ABI tl_fuzz_ev with host buffers: pinned host seeds -> GPU (H2D), "
+                        "ordered event lists written by k_scan_emit into pinned host memory "
+                        "(zero-copy), labels D2H (N>1: after the NCCL all-gather; histogram D2H)",
                 "with_records": {"value": e2r_recs_all / t_e2r, "unit": "env-steps/s",
                                  "d2h_bytes_per_step": d2h_rb,
                                  "note": "same, plus tl_scan_counts + tl_compact_records into one "
