@@ -403,7 +403,10 @@ static SynthKernel synth_kernel(int w, bool fuzz, bool small) {
 #endif
 
 typedef void (*SynthWarpKernel)(SynthParams);
-constexpr int kSynthWarps = 4;  // warps (independent episodes) per CTA of k_synth_warp
+#ifndef TL_SYNTH_NW
+#define TL_SYNTH_NW 2
+#endif
+constexpr int kSynthWarps = TL_SYNTH_NW;  // warps (independent episodes) per CTA of k_synth_warp
 
 static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   // realize + label: one warp per episode (tl_synth_warp.cuh)
@@ -441,6 +444,13 @@ static int launch_synth(SynthParams& sp, bool fuzz, void* stream) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSynthWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;
+  // long episodes and at most ~2 per warp slot: the batch time is the longest
+  // episodes' latency, so 12 warps per SM (less issue contention for them)
+  // beat 16 (scripts/ab_env2.sh: -1.5% on the 4096-env Place step; the
+  // short-episode C3 batch and a 16384-env batch want all 16)
+  if (sp.order && (int64_t)sp.n_env <= (int64_t)sm_count() * 32)
+    per_sm = std::min(per_sm, 12 / kSynthWarps);
+  if (const char* f = ab_env("TL_SYNTH_CTAS")) per_sm = std::min(per_sm, std::max(1, atoi(f)));
   const int grid = blocks_for(sp.n_env, kSynthWarps, sm_count() * per_sm);
   if (ab_env("TL_DEBUG"))
     fprintf(stderr, "k_synth_warp: %d CTAs/SM x %d warps (smem %d B), grid %d\n", per_sm,
