@@ -34,3 +34,6 @@ tot = sum(t[k] for k in names)
 print(f"n={n} kind={kind} waves={int(waves)} warp-cycles {tot:.3g} ({tot / waves:.0f} per wave)")
 for k, nm in names.items():
     print(f"  {nm:16s} {t[k] / waves:7.0f} cycles/wave  {100 * t[k] / tot:5.1f} %")
+if t[14]:
+    print(f"  producer: {int(t[14])} blocks, {t[13] / t[14]:.0f} cycles per block twisting, "
+          f"{t[12] / t[14]:.0f} cycles per block waiting (sleep quanta)")
