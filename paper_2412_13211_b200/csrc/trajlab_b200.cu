@@ -693,7 +693,8 @@ int tl_env_step(void* state, int32_t n_env, int32_t dof, const uint8_t* actions,
   ep.step_mask = step_mask;
   // 8 lanes per env while the batch leaves SMs idle (latency-bound), 4 when
   // it fills the GPU (less redundant per-env planning); 16 measured slower
-  const bool wide = (int64_t)n_env * 8 <= (int64_t)sm_count() * 1024;
+  bool wide = (int64_t)n_env * 8 <= (int64_t)sm_count() * 1024;
+  if (const char* f = ab_env("TL_ENV_LPE")) wide = atoi(f) == 8;
   auto go = [&](auto kern, int lpe, size_t smem) {
     set_max_smem(kern, (int)smem);
     const int per_block = kEnvQThreads / lpe;
