@@ -26,6 +26,32 @@ __device__ unsigned long long g_tl_prof[128];
 #define TL_STAMP(i) do { } while (0)
 #endif
 
+#ifdef TL_PHASES
+// step timeline of the last launches (profiling build only,
+// scripts/step_timeline.py): [kernel][block] = {first start, last end}
+// (globaltimer ns); kernel 0 = fuzz reset, 1 = k_scan_emit
+__device__ unsigned long long g_tl_step[2][2048][2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct BlockSpan {  // start at construction, end (max over warps) at scope exit
+  int k;
+  __device__ explicit BlockSpan(int kk) : k(kk) {
+    if (blockIdx.x < 2048 && (threadIdx.x & 31) == 0)
+      atomicMin(&g_tl_step[k][blockIdx.x][0], gtimer());
+  }
+  __device__ ~BlockSpan() {
+    if (blockIdx.x < 2048 && (threadIdx.x & 31) == 0)
+      atomicMax(&g_tl_step[k][blockIdx.x][1], gtimer());
+  }
+};
+#define TL_BLOCK_SPAN(k) BlockSpan tl_span_(k)
+#else
+#define TL_BLOCK_SPAN(k) do { } while (0)
+#endif
+
 // Bounds / invariant checks of the checked build (-DTL_CHECK,
 // scripts/gpu_check_build.sh): a failing check prints its site and traps
 // (the CUDA context dies, the calling test fails loudly).  compute-sanitizer

@@ -1282,14 +1282,78 @@ __global__ void __launch_bounds__(256)
 
 namespace tl {
 
+// k_scan_emit's per-episode body: warp `warp` of the block writes episode e's
+// ordered (kind, t) list at out_kind / out_t + base (global, or the tile's
+// shared staging area with base relative to the tile)
+__device__ __forceinline__ void emit_tile_lists(const uint8_t* __restrict__ step_mask,
+                                                const int64_t* __restrict__ rec_start,
+                                                const int32_t* __restrict__ n_rec,
+                                                const tl_label* __restrict__ labels, int n_env,
+                                                int e, int64_t base, uint8_t* out_kind,
+                                                int32_t* out_t) {
+  const int lane = lane_id();
+  if (e >= n_env || labels[e].n_events == 0) return;
+  const int sub = labels[e].subtask;
+  const int64_t rs = rec_start[e];
+  const int n = n_rec[e];
+  TL_ASSERT(rs >= 0 && n >= 0);
+  // four records per lane (one 32-bit load when the episode's masks are
+  // 4-byte aligned), up to eight 128-record chunks loaded before any is
+  // processed: the longest episode's chain of dependent loads sets the time
+  const uint8_t* sm = step_mask + rs;
+  const bool al = (reinterpret_cast<uintptr_t>(sm) & 3) == 0;
+  for (int c0 = 0; c0 < n; c0 += 1024) {
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int t = c0 + 128 * k + 4 * lane;
+      uint32_t v = 0u;
+      if (al && t + 3 < n) {
+        v = *reinterpret_cast<const uint32_t*>(sm + t);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; b++)
+          if (t + b < n) v |= (uint32_t)sm[t + b] << (8 * b);
+      }
+      w[k] = v;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (c0 + 128 * k >= n) break;  // warp-uniform
+      const int t4 = c0 + 128 * k + 4 * lane;
+      const uint32_t v = w[k];
+      const int cnt = __popc(v);
+      const int incl = warp_incl_scan(cnt);
+      int64_t pos = base + incl - cnt;
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        uint32_t m = (v >> (8 * b)) & 0xffu;
+        while (m) {
+          const int q = __ffs(m) - 1;
+          m &= m - 1;
+          out_kind[pos] = kAlpha[sub][q];
+          out_t[pos] = t4 + b;
+          pos++;
+        }
+      }
+      base += __shfl_sync(kFull, incl, 31);
+    }
+  }
+}
+
 // ---- K2 fused: event-offset scan (decoupled look-back) + event emission -------
 // One block = 32 warps = a tile of 32 episodes.  Warp 0 scans the tile's
 // n_events, publishes the tile aggregate and walks back over predecessor
 // tiles (tiles are taken in launch order through a ticket counter, so a
 // predecessor is always resident or finished); then warp w emits episode w
 // of the tile.  Replaces scan (3 launches) + emit (1 launch) by one.
+// A tile's events are one contiguous range of the output: when they fit the
+// shared staging area the warps write them there and the block stores the
+// range with contiguous, fully used lines (the event lists may live in pinned
+// host memory, where scattered 1- and 4-byte stores each cost a PCIe write).
 constexpr uint64_t kTileAgg = 1ull << 62, kTilePrefix = 2ull << 62;
 constexpr uint64_t kTileValMask = (1ull << 62) - 1;
+constexpr int kEvStage = 4096;  // events staged per tile (20 KB)
 
 __global__ void __launch_bounds__(1024)
     k_scan_emit(const uint8_t* __restrict__ step_mask, const int64_t* __restrict__ rec_start,
@@ -1298,6 +1362,10 @@ __global__ void __launch_bounds__(1024)
                 int32_t* __restrict__ ev_t, unsigned long long* tile_state) {
   __shared__ int s_tile;
   __shared__ int64_t s_off[32];
+  __shared__ int64_t s_tot;
+  __shared__ __align__(16) int32_t s_t[kEvStage + 4];
+  __shared__ __align__(16) uint8_t s_k[kEvStage + 4];
+  TL_BLOCK_SPAN(1);
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int n_tiles = (n_env + 31) / 32;
   if (threadIdx.x == 0)
@@ -1343,57 +1411,48 @@ __global__ void __launch_bounds__(1024)
     prefix = __shfl_sync(kFull, prefix, 0);
     const int64_t off = prefix + incl - cnt;
     s_off[lane] = off;
+    if (lane == 0) s_tot = total;
     if (e < n_env) ev_off[e] = off;
     if (e == n_env - 1) ev_off[n_env] = off + cnt;
   }
   __syncthreads();
-  const int e = tile * 32 + warp;
-  if (e >= n_env || labels[e].n_events == 0) return;
-  const int sub = labels[e].subtask;
-  const int64_t rs = rec_start[e];
-  const int n = n_rec[e];
-  TL_ASSERT(rs >= 0 && n >= 0);
-  int64_t base = s_off[warp];
-  // four records per lane (one 32-bit load when the episode's masks are
-  // 4-byte aligned), up to eight 128-record chunks loaded before any is
-  // processed: the longest episode's chain of dependent loads sets the time
-  const uint8_t* sm = step_mask + rs;
-  const bool al = (reinterpret_cast<uintptr_t>(sm) & 3) == 0;
-  for (int c0 = 0; c0 < n; c0 += 1024) {
-    uint32_t w[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int t = c0 + 128 * k + 4 * lane;
-      uint32_t v = 0u;
-      if (al && t + 3 < n) {
-        v = *reinterpret_cast<const uint32_t*>(sm + t);
+  const int64_t tile_base = s_off[0];
+  const int64_t tile_tot = s_tot;
+  const bool staged = tile_tot <= kEvStage && (reinterpret_cast<uintptr_t>(ev_t) & 3u) == 0;
+  // staged at the output's phase within a 16-byte (times) / 4-byte (kinds)
+  // word, so the copy-out stores whole aligned words from aligned words
+  int32_t* gt = ev_t + tile_base;
+  uint8_t* gk = ev_kind + tile_base;
+  const int sh_t = (int)((reinterpret_cast<uintptr_t>(gt) >> 2) & 3u);
+  const int sh_k = (int)(reinterpret_cast<uintptr_t>(gk) & 3u);
+  emit_tile_lists(step_mask, rec_start, n_rec, labels, n_env, tile * 32 + warp,
+                  staged ? s_off[warp] - tile_base : s_off[warp],
+                  staged ? s_k + sh_k : ev_kind, staged ? s_t + sh_t : ev_t);
+  if (!staged) return;
+  __syncthreads();
+  const int n = (int)tile_tot;
+  {
+    int4* gw = reinterpret_cast<int4*>(gt - sh_t);
+    const int4* sw = reinterpret_cast<const int4*>(s_t);
+    const int end = sh_t + n;
+    for (int v = threadIdx.x; 4 * v < end; v += blockDim.x) {
+      if (4 * v >= sh_t && 4 * v + 4 <= end) {
+        gw[v] = sw[v];
       } else {
-#pragma unroll
-        for (int b = 0; b < 4; b++)
-          if (t + b < n) v |= (uint32_t)sm[t + b] << (8 * b);
+        for (int j = max(4 * v, sh_t); j < min(4 * v + 4, end); j++) (gt - sh_t)[j] = s_t[j];
       }
-      w[k] = v;
     }
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      if (c0 + 128 * k >= n) break;  // warp-uniform
-      const int t4 = c0 + 128 * k + 4 * lane;
-      const uint32_t v = w[k];
-      const int cnt = __popc(v);
-      const int incl = warp_incl_scan(cnt);
-      int64_t pos = base + incl - cnt;
-#pragma unroll
-      for (int b = 0; b < 4; b++) {
-        uint32_t m = (v >> (8 * b)) & 0xffu;
-        while (m) {
-          const int q = __ffs(m) - 1;
-          m &= m - 1;
-          ev_kind[pos] = kAlpha[sub][q];
-          ev_t[pos] = t4 + b;
-          pos++;
-        }
+  }
+  {
+    uint32_t* gw = reinterpret_cast<uint32_t*>(gk - sh_k);
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(s_k);
+    const int end = sh_k + n;
+    for (int v = threadIdx.x; 4 * v < end; v += blockDim.x) {
+      if (4 * v >= sh_k && 4 * v + 4 <= end) {
+        gw[v] = sw[v];
+      } else {
+        for (int j = max(4 * v, sh_k); j < min(4 * v + 4, end); j++) (gk - sh_k)[j] = s_k[j];
       }
-      base += __shfl_sync(kFull, incl, 31);
     }
   }
 }

@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(E * 32) k_fuzz_reset_cta(SynthParams p) {
   extern __shared__ uint32_t rows[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t e0 = (int64_t)blockIdx.x * E;
+  TL_BLOCK_SPAN(0);
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.tickets) reset_counters(p);
   if (threadIdx.x == 0) TL_STAMP(0);
   if (warp == 0) {

@@ -151,11 +151,6 @@ __device__ unsigned long long g_tl_wphase[16];  // clock64 deltas summed over wa
     if (lane == 0) atomicAdd(&g_tl_wphase[(k)], (unsigned long long)(_t - ph_t));   \
     ph_t = _t;                                                                      \
   } while (0)
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 #else
 #define TL_WPH(k) do { } while (0)
 #endif

@@ -897,6 +897,16 @@ int tl_compact_records(const tl_records* src, int32_t n_env, const int64_t* dst_
 extern "C" int tl_warp_timeline(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tl_warp, sizeof(g_tl_warp)) == cudaSuccess ? TL_OK : TL_E_CUDA;
 }
+extern "C" int tl_step_timeline(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_tl_step, sizeof(g_tl_step)) != cudaSuccess) return TL_E_CUDA;
+  if (reset) {  // starts to +inf, ends to 0
+    static unsigned long long z[2][2048][2];
+    for (int k = 0; k < 2; k++)
+      for (int b = 0; b < 2048; b++) z[k][b][0] = ~0ull, z[k][b][1] = 0ull;
+    if (cudaMemcpyToSymbol(g_tl_step, z, sizeof(z)) != cudaSuccess) return TL_E_CUDA;
+  }
+  return TL_OK;
+}
 extern "C" int tl_warp_phases(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_tl_wphase, sizeof(g_tl_wphase)) != cudaSuccess) return TL_E_CUDA;
   if (reset) {

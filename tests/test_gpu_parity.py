@@ -394,6 +394,57 @@ def test_fused_scan_emit_matches_two_pass(C, TH, kind):
     assert torch.equal(a.ev_t[:tot], b.ev_t[:tot])
 
 
+@pytest.mark.parametrize("density", [0.05, 0.9])
+@pytest.mark.parametrize("shift", [0, 1, 3])
+def test_scan_emit_staging_and_alignment(C, TH, density, shift):
+    """k_scan_emit stages a tile's events in shared memory and stores the
+    tile's range with aligned words: sparse masks take the staged path, dense
+    masks (> 4096 events per 32-episode tile) the direct one; outputs offset
+    by `shift` elements move every tile's phase.  Against the two-pass
+    tl_scan_events + tl_emit_events on the same masks."""
+    from paper_2412_13211_b200 import _lib as L
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_gap=64, max_tail=64)
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 700
+    sb = C.fuzz_batch(np.arange(n) + 31337, 0, cfg, TH(), cs)
+    rng = np.random.default_rng(int(density * 100) + shift)
+    nbits = int(sb.step_mask.numel())
+    bits = (rng.random((nbits, 8)) < density).astype(np.uint8)
+    mask_np = (bits << np.arange(8, dtype=np.uint8)).sum(axis=1).astype(np.uint8)
+    rs = sb.records.rec_start.cpu().numpy()
+    nr = sb.records.n_rec.cpu().numpy()
+    pop = np.unpackbits(mask_np[:, None], axis=1).sum(axis=1)
+    for e in range(n):  # record 0 never carries an edge; keep the masks inside the episodes
+        mask_np[rs[e]] = 0
+        pop[rs[e]] = 0
+    lab = sb.labels.clone()
+    lv = lab.cpu().numpy().reshape(-1).view(np.dtype([("status", "<i4"), ("n_events", "<i4"), ("err", "<i4"), ("sub", "u1"), ("mode", "u1"), ("flags", "u1"), ("pad", "u1"), ("d0", "<f8")]))
+    lv["n_events"] = [int(pop[rs[e]:rs[e] + nr[e]].sum()) for e in range(n)]
+    lv["sub"] = np.arange(n) % 4
+    lab = torch.from_numpy(lv.view(np.uint8).reshape(lab.shape)).cuda()
+    mask = torch.from_numpy(mask_np).cuda()
+    a = C.LabelResult(lab, mask, None)
+    C.emit_events(sb.records, a)
+    tot = int(a.ev_off[-1])
+    if density > 0.5:
+        assert tot > 4096 * (n // 32)  # the direct path on every full tile
+    ev_off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    kbuf = torch.full((tot + 8,), 0xAB, dtype=torch.uint8, device="cuda")
+    tbuf = torch.full((tot + 8,), -7, dtype=torch.int32, device="cuda")
+    scratch = torch.empty(max(16, L.lib().tl_scan_scratch_bytes(n)), dtype=torch.uint8, device="cuda")
+    L.check(L.lib().tl_scan_emit_events(L.ptr(mask), L.ptr(sb.records.rec_start),
+                                        L.ptr(sb.records.n_rec), L.ptr(lab), n, L.ptr(ev_off),
+                                        kbuf.data_ptr() + shift, tbuf.data_ptr() + 4 * shift,
+                                        L.ptr(scratch), L.stream_ptr()), "tl_scan_emit_events")
+    assert torch.equal(ev_off, a.ev_off)
+    assert torch.equal(kbuf[shift:shift + tot], a.ev_kind[:tot])
+    assert torch.equal(tbuf[shift:shift + tot], a.ev_t[:tot])
+    # nothing outside [shift, shift + tot) was written
+    assert bool((kbuf[:shift] == 0xAB).all()) and bool((kbuf[shift + tot:] == 0xAB).all())
+    assert bool((tbuf[:shift] == -7).all()) and bool((tbuf[shift + tot:] == -7).all())
+
+
 @pytest.mark.parametrize("kind", range(4))
 @pytest.mark.parametrize("n", [1, 37, 5000])
 def test_fused_synth_events_match_two_pass(C, TH, kind, n):
