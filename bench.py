@@ -557,7 +557,7 @@ def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
             "parity": "tests/test_gpu_shipped.py::test_c5_bench_scale_filter_vs_oracle"}
 
 
-def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None):
+def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None, seeds_host=None):
     """One fused fuzz step (tl_fuzz_ev: reset + realize + labels + ordered
     event lists) on preallocated buffers, captured as a CUDA graph.  host_out
     (pinned host tensors ev_off / ev_kind / ev_t, optionally labels): the
@@ -565,6 +565,8 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None):
     io (pinned host tensors seeds [n] int64, labels [n, 24] u8): the graph
     also copies the seeds in (H2D) and the labels out (D2H), so one graph
     launch is the whole host-to-host step.
+    seeds_host (pinned host int64 [n]): the reset kernel reads the seeds
+    straight from host memory (zero-copy H2D inside the step).
     Returns (graph, seeds_buf, workspace, device event buffers)."""
     import ctypes
     import torch
@@ -592,7 +594,7 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None):
     def body(s):
         if io is not None:
             seeds_buf.copy_(io["seeds"], non_blocking=True)
-        L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf), n_env, kind, ctypes.byref(cfg_c),
+        L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf if seeds_host is None else seeds_host), n_env, kind, ctypes.byref(cfg_c),
                                ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
                                None, None, None, L.ptr(ws.step_mask), L.ptr(out["labels"]),
                                L.ptr(out["ev_off"]), L.ptr(out["ev_kind"]), L.ptr(out["ev_t"]),
@@ -605,7 +607,7 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         body(torch.cuda.current_stream())
-    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf, out)  # the graph reads these
+    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf, out, seeds_host)  # the graph reads these
     return g, seeds_buf, ws, bufs
 
 
@@ -756,12 +758,12 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
             "progressive_completion": curve}
 
 
-def self_check(ws, ev_host, seeds):
+def self_check(ws, ev_host, seeds, labels=None):
     """the timed kernels' last outputs against the CPU oracle (oracle/, test
     infrastructure): every label field and the ordered event lists"""
     from oracle import oracle as O
     from paper_2412_13211_b200 import _lib as L
-    lab = ws.labels.cpu().numpy().reshape(-1).view(L.LABEL_DTYPE)
+    lab = (ws.labels if labels is None else labels).cpu().numpy().reshape(-1).view(L.LABEL_DTYPE)
     nrec = ws.n_rec.cpu().numpy()
     want = O.fuzz_label_batch_full(int(seeds[0]), len(seeds), KIND, oracle_cfg(),
                                    n_threads=os.cpu_count() or 1)
@@ -816,9 +818,20 @@ def main(argv=None):
                    ev_t=torch.empty(ev_cap, dtype=torch.int32).pin_memory())
     graph, seeds_buf, ws, ev_dev = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg)
     graph_h, seeds_h, ws_h, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg, host_out=ev_host)
-    # (capturing the H2D / D2H copies into the step graph measured 3-5% slower
-    # end to end than separate async copies: scripts/e2e_variants.py)
-    io = None
+    # one GPU: zero-copy both ways -- the reset kernel reads the seeds from the
+    # pinned staging buffer, the realize kernel writes the labels and
+    # k_scan_emit the event lists into pinned memory (scripts/e2e_variants.py:
+    # 135 us per step vs 147-152 us with copy_ H2D + D2H around the graph; the
+    # copies captured into the graph measured slower still).  N > 1 keeps the
+    # labels on the device for the NCCL all-gather and copies them back.
+    zc = None
+    if world == 1:
+        zc_seeds = torch.empty(N_ENV, dtype=torch.int64).pin_memory()
+        zc_labels = torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory()
+        graph_zc, _, ws_zc, _ = fuzz_step_graph(dev, stream, N_ENV, KIND, cfg,
+                                                host_out=dict(ev_host, labels=zc_labels),
+                                                seeds_host=zc_seeds)
+        zc = (graph_zc, ws_zc, zc_seeds.numpy(), zc_labels)
     hist = torch.zeros(L.N_MODES, dtype=torch.int64, device=dev)
     gathered = torch.empty((world * N_ENV, 24), dtype=torch.uint8, device=dev)
     # inputs resident in HBM: seeds of every step, rank-disjoint ranges
@@ -883,6 +896,7 @@ def main(argv=None):
         # contiguous staging buffer [23 planes x R f32 | R grasped u8] and ONE
         # D2H copy of it (+ the record offsets).
         host_seeds = all_seeds.cpu().pin_memory()
+        hs_np = host_seeds.numpy()
         h_labels = torch.empty((N_ENV, 24), dtype=torch.uint8).pin_memory()
         h_hist = torch.empty(L.N_MODES, dtype=torch.int64).pin_memory()
         h_tot = torch.empty(1, dtype=torch.int64).pin_memory()
@@ -900,9 +914,9 @@ def main(argv=None):
             for k in range(K2):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                if io is not None and not with_records:
-                    io["seeds"].copy_(host_seeds[k])      # this step's inputs, pinned staging
-                    graph_io.replay()                     # H2D seeds, fuzz_ev, D2H labels
+                if zc is not None and not with_records:
+                    np.copyto(zc[2], hs_np[k])  # this step's inputs into the staging the kernel reads
+                    zc[0].replay()              # seeds over PCIe, labels + event lists back
                     stream.synchronize()
                     wall += time.perf_counter() - t0
                     NE = int(ev_host["ev_off"][N_ENV])
@@ -946,9 +960,8 @@ def main(argv=None):
             return wall, recs, h2d, d2h
 
         t_e2e, e2e_recs, h2d_b, d2h_b = e2e_loop(False)
-        check = self_check(ws_io if io is not None else ws_h, ev_host, host_seeds[K2 - 1].numpy())
-        if io is not None and not torch.equal(io["labels"], ws_io.labels.cpu()):
-            raise RuntimeError("bench self-check: the D2H label copy differs from the device labels")
+        check = self_check(zc[1] if zc else ws_h, ev_host, hs_np[K2 - 1],
+                           labels=zc[3] if zc else None)
         t_e2r, e2r_recs, _, d2h_rb = e2e_loop(True)
         extras = {}
         if not args.no_extras:
@@ -1025,9 +1038,11 @@ def main(argv=None):
                 "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": K2,
                 "timing": "time.perf_counter around the calls + stream synchronize, per step, "
                           "max over ranks",
-                "note": "C-ABI tl_fuzz_ev with host buffers: pinned host seeds -> GPU (H2D), "
-                        "ordered event lists written by k_scan_emit into pinned host memory "
-                        "(zero-copy), labels D2H (N>1: after the NCCL all-gather; histogram D2H)",
+                "note": "C-ABI tl_fuzz_ev with host buffers: the step's seeds copied into a "
+                        "pinned staging buffer that the reset kernel reads over PCIe, labels "
+                        "(realize kernel) and ordered event lists (k_scan_emit) written into "
+                        "pinned host memory (zero-copy); N>1: seeds H2D, labels on the device "
+                        "for the NCCL all-gather, then labels + histogram D2H",
                 "with_records": {"value": e2r_recs_all / t_e2r, "unit": "env-steps/s",
                                  "d2h_bytes_per_step": d2h_rb,
                                  "note": "same, plus tl_scan_counts + tl_compact_records into one "

@@ -25,6 +25,13 @@ io = dict(seeds=torch.empty(N, dtype=torch.int64).pin_memory(),
 io_np = io["seeds"].numpy()
 g_h, seeds_h, ws_h, _ = bench.fuzz_step_graph(dev, stream, N, KIND, cfg, host_out=ev_host)
 g_io, _, ws_io, _ = bench.fuzz_step_graph(dev, stream, N, KIND, cfg, host_out=ev_host, io=io)
+# zero-copy both ways: the reset kernel reads the pinned seeds, the realize
+# kernel writes the labels and k_scan_emit the event lists into pinned memory
+zc_seeds = torch.empty(N, dtype=torch.int64).pin_memory()
+zc_np = zc_seeds.numpy()
+zc_out = dict(ev_host, labels=torch.empty((N, 24), dtype=torch.uint8).pin_memory())
+g_zc, _, ws_zc, _ = bench.fuzz_step_graph(dev, stream, N, KIND, cfg, host_out=zc_out,
+                                          seeds_host=zc_seeds)
 
 
 def run(name, step):
@@ -56,6 +63,19 @@ def c(k):
     stream.synchronize()
 
 
+def e(k):
+    np.copyto(zc_np, hs_np[k])
+    g_zc.replay()
+    stream.synchronize()
+
+
+def f(k):
+    np.copyto(zc_np, hs_np[k])
+    g_zc.replay()
+    h_labels.copy_(ws_zc.labels, non_blocking=True)
+    stream.synchronize()
+
+
 def d(k):
     g_h.replay()
     stream.synchronize()
@@ -66,3 +86,13 @@ for _ in range(2):
     run("b: torch host copy + graph(io)", b)
     run("c: numpy host copy + graph(io)", c)
     run("d: graph only (device seeds, no D2H)", d)
+    run("e: zero-copy seeds + labels + events", e)
+    run("f: zero-copy seeds, labels D2H copy", f)
+np.copyto(zc_np, hs_np[3])
+g_zc.replay()
+stream.synchronize()
+ref = bench.fuzz_step_graph(dev, stream, N, KIND, cfg)
+ref[1].copy_(torch.from_numpy(hs_np[3]).to(dev))
+ref[0].replay()
+torch.cuda.synchronize()
+print("zero-copy labels == device labels:", torch.equal(zc_out["labels"], ref[2].labels.cpu()))
