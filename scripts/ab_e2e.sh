@@ -10,7 +10,7 @@ done
 for round in 1 2; do
 for m in ${VARIANTS:-base}; do
   cp scripts/_ab/$m.so paper_2412_13211_b200/libtrajlab_b200.so
-  echo "$m | $(python scripts/headline_step.py 20 2>&1 | tail -1 | cut -d' ' -f3) | $(python scripts/e2e_variants.py 2>&1 | grep -E '^(a|d):' | tail -2 | awk '{print $1, $(NF-4)}' | tr '\n' ' ')"
+  echo "$m | $(python scripts/headline_step.py 20 2>&1 | tail -1 | cut -d' ' -f3) | $(python scripts/e2e_variants.py 2>&1 | grep -E '^(a|d|e):' | tail -3 | awk '{print $1, $(NF-4)}' | tr '\n' ' ')"
 done
 done
 cp /tmp/orig.so paper_2412_13211_b200/libtrajlab_b200.so
