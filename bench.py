@@ -997,6 +997,15 @@ def main(argv=None):
     crit_cycles = 1247 * c_seed + max_rec * c_cum
     floor_s = crit_cycles / (sm_ghz * 1e9)
     prof = profile_json("r2_ncu_headline.json") or {}
+    # dependency + issue floor: the realize kernel cannot start before the
+    # reset's seeding chains end (longest-first claims need every script), and
+    # the realize + event-list kernels cannot finish before every SM scheduler
+    # has issued their warp instructions at one per cycle (ncu counts, same config)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    inst_after = sum(k["warp_instructions"] for k in prof.get("kernels", [])
+                     if "k_synth_warp" in k["kernel"] or "k_scan_emit" in k["kernel"])
+    issue_floor_s = (1247 * c_seed / (sm_ghz * 1e9) + inst_after / (4 * n_sm * sm_ghz * 1e9)) \
+        if inst_after else None
     sps = total_recs / t_dev
     cb_sps, cb_eps, cb_sample = cpu_baseline(args.cpu_seconds)
     pyref = python_reference_baseline()
@@ -1029,6 +1038,12 @@ def main(argv=None):
             "realize_kernel": prof.get("realize_kernel"),
             "note": ("floor = one episode's serial chains; the batch is also issue-bound: the "
                      "realize kernel's issue_active (ncu, same config) says how full the SMs are"),
+            "issue_floor": None if issue_floor_s is None else {
+                "floor_ms": 1e3 * issue_floor_s, "frac": issue_floor_s / step_s,
+                "warp_instructions": inst_after, "schedulers": 4 * n_sm,
+                "model": ("1247 seeding steps (the reset's chain: the realize kernel needs every "
+                          "script) + the realize and event-list kernels' warp instructions "
+                          "(profiles/r2_ncu_headline.json) issued at 1 per scheduler per cycle")},
             "hbm": {"achieved": alg_bytes / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": alg_bytes / step_s / 1e9 / hbm_peak, "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": alg_bytes,
