@@ -54,6 +54,11 @@ for rep in range(6):
     w = wt[wt[:, 3] > 0].astype(np.float64)
     t0 = r[:, 0].min()
     f = lambda a: (a - t0) / 1e3
+    if rep == 5:
+        sp = f(r[:, 1]) - f(r[:, 0])
+        print("  reset block starts p50/p90/max %.1f/%.1f/%.1f us, spans p10/p50/p90/max %.1f/%.1f/%.1f/%.1f us" % (
+            np.percentile(f(r[:, 0]), 50), np.percentile(f(r[:, 0]), 90), f(r[:, 0]).max(),
+            np.percentile(sp, 10), np.percentile(sp, 50), np.percentile(sp, 90), sp.max()))
     rows.append([f(r[:, 1]).max(), f(r[:, 1]).min(), np.median(f(r[:, 1]) - f(r[:, 0])),
                  f(w[:, 0]).min(), f(w[:, 0]).max(), np.percentile(f(w[:, 1]), 90), f(w[:, 1]).max(),
                  f(s[:, 0]).min(), f(s[:, 0]).max(), f(s[:, 1]).max()])
