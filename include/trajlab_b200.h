@@ -257,8 +257,11 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask,
 
 /* tl_fuzz + the ordered event lists: ev_off[n+1], (ev_kind, ev_t) at
  * ev_off[e] exactly as tl_scan_emit_events produces them (the reset, realize
- * and k_scan_emit kernels back to back on `stream`; the outputs may be
- * pinned host memory).  step_mask is required;
+ * and k_scan_emit kernels back to back on `stream`).  seeds, labels, ev_off,
+ * ev_kind and ev_t may be pinned (mapped) host memory: the reset kernel reads
+ * the seeds, the realize kernel writes each label once, and each
+ * 32-episode tile's events are stored as one contiguous range of aligned
+ * words (zero-copy end to end, bench.py e2e).  step_mask is required;
  * ev_capacity >= 4 * n_env * cap_per_env. */
 int tl_fuzz_ev(const int64_t* seeds, int32_t n_env, int32_t subtask,
                const tl_fuzz_cfg* cfg /* host */,

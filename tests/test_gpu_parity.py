@@ -470,8 +470,9 @@ def test_fused_synth_events_match_two_pass(C, TH, kind, n):
 
 
 def test_fused_events_zero_copy_host_outputs(C, TH):
-    """tl_fuzz_ev writing labels and event lists straight into pinned host
-    memory (the e2e path) == the device-memory outputs."""
+    """tl_fuzz_ev reading the seeds from and writing labels and event lists
+    straight into pinned host memory (the e2e path) == the device-memory
+    outputs."""
     import ctypes
     from paper_2412_13211_b200 import _lib as L
     from paper_2412_13211_b200.synth import FuzzConfig
@@ -489,7 +490,8 @@ def test_fused_events_zero_copy_host_outputs(C, TH):
     h_k = torch.empty(ev_cap, dtype=torch.uint8).pin_memory()
     h_t = torch.empty(ev_cap, dtype=torch.int32).pin_memory()
     rb = ws.records()
-    rc = L.lib().tl_fuzz_ev(L.ptr(seeds), n, 1, ctypes.byref(C.fuzz_cfg_c(cfg)),
+    h_seeds = seeds.cpu().pin_memory()
+    rc = L.lib().tl_fuzz_ev(L.ptr(h_seeds), n, 1, ctypes.byref(C.fuzz_cfg_c(cfg)),
                             ctypes.byref(C.thresholds_c(TH())), L.ptr(cs), None,
                             ctypes.byref(rb.c()), cap, None, None, None, L.ptr(ws.step_mask),
                             L.ptr(h_lab), L.ptr(h_off), L.ptr(h_k), L.ptr(h_t), ev_cap,
