@@ -557,7 +557,8 @@ def c5_run(dev, stream, world, n_per_subtask=250_000, reps=3):
             "parity": "tests/test_gpu_shipped.py::test_c5_bench_scale_filter_vs_oracle"}
 
 
-def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None, seeds_host=None):
+def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None, seeds_host=None,
+                    subtasks=None):
     """One fused fuzz step (tl_fuzz_ev: reset + realize + labels + ordered
     event lists) on preallocated buffers, captured as a CUDA graph.  host_out
     (pinned host tensors ev_off / ev_kind / ev_t, optionally labels): the
@@ -567,6 +568,8 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None, seeds
     launch is the whole host-to-host step.
     seeds_host (pinned host int64 [n]): the reset kernel reads the seeds
     straight from host memory (zero-copy H2D inside the step).
+    subtasks (device u8 [n]): a subtask per episode (tl_fuzz_ev_mixed; kind
+    is then ignored).
     Returns (graph, seeds_buf, workspace, device event buffers)."""
     import ctypes
     import torch
@@ -594,7 +597,10 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None, seeds
     def body(s):
         if io is not None:
             seeds_buf.copy_(io["seeds"], non_blocking=True)
-        L.check(lib.tl_fuzz_ev(L.ptr(seeds_buf if seeds_host is None else seeds_host), n_env, kind, ctypes.byref(cfg_c),
+        sp = L.ptr(seeds_buf if seeds_host is None else seeds_host)
+        head = (sp, L.ptr(subtasks), n_env) if subtasks is not None else (sp, n_env, kind)
+        fn = lib.tl_fuzz_ev_mixed if subtasks is not None else lib.tl_fuzz_ev
+        L.check(fn(*head, ctypes.byref(cfg_c),
                                ctypes.byref(th_c), L.ptr(cs), None, ctypes.byref(rb_c), cap,
                                None, None, None, L.ptr(ws.step_mask), L.ptr(out["labels"]),
                                L.ptr(out["ev_off"]), L.ptr(out["ev_kind"]), L.ptr(out["ev_t"]),
@@ -607,7 +613,7 @@ def fuzz_step_graph(dev, stream, n_env, kind, cfg, host_out=None, io=None, seeds
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         body(torch.cuda.current_stream())
-    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf, out, seeds_host)  # the graph reads these
+    ws._keep = (cs, th_c, cfg_c, bufs, rb_c, seeds_buf, out, seeds_host, subtasks)  # the graph reads these
     return g, seeds_buf, ws, bufs
 
 
@@ -701,8 +707,9 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
     """C4: SetTable chains, 4096 per GPU; chain c runs Open,
     Pick, Place, Close twice with seeds 8c + k (k = 0..7); slot success =
     success_once; progressive_completion over the 16-slot settable plan
-    (alive counts all-reduced over ranks).  One fused fuzz graph per subtask
-    (both repetitions, 8192 episodes), then tl_chain_progress."""
+    (alive counts all-reduced over ranks).  One fused fuzz graph over all
+    8 episodes of every chain (tl_fuzz_ev_mixed: a subtask per episode,
+    episode 8c + k), then tl_chain_progress."""
     import torch
     import paper_2412_13211_b200 as P
     from paper_2412_13211_b200 import _lib as L
@@ -711,23 +718,20 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
     plan = BUILTIN_PLANS["settable"]
     c0 = rank * n_chain
     cfg = P.FuzzConfig()
-    order = {"Open": 0, "Pick": 1, "Place": 2, "Close": 3}   # k within a repetition
+    order = ["Open", "Pick", "Place", "Close"]   # k % 4 within a repetition (k // 4)
     sub_idx = {"Pick": 0, "Place": 1, "Open": 2, "Close": 3}
+    ks = torch.arange(8, device=dev)
+    subtasks = torch.tensor([sub_idx[order[k % 4]] for k in range(8)], dtype=torch.uint8,
+                            device=dev).repeat(n_chain)
+    g, seeds_buf, ws, _ = fuzz_step_graph(dev, stream, 8 * n_chain, 0, cfg, subtasks=subtasks)
     chains = torch.arange(c0, c0 + n_chain, dtype=torch.int64, device=dev)
-    subs = ["Open", "Pick", "Place", "Close"]
-    graphs = []
-    for si, sub in enumerate(subs):   # label rows [2n*si, 2n*(si+1)): rep 0 then rep 1
-        g, seeds_buf, ws, _ = fuzz_step_graph(dev, stream, 2 * n_chain, sub_idx[sub], cfg)
-        seeds_buf.copy_(torch.cat([8 * chains + 4 * rep + order[sub] for rep in (0, 1)]))
-        graphs.append((g, ws))
+    seeds_buf.copy_((8 * chains[:, None] + ks[None, :]).reshape(-1))
     slot_label = torch.full((n_chain, len(plan)), -1, dtype=torch.int64, device=dev)
     for j, slot in enumerate(plan.slots):
         if slot.auto_success:
             continue
         rep = 0 if j < 8 else 1
-        slot_label[:, j] = (2 * subs.index(slot.subtask) + rep) * n_chain + \
-            torch.arange(n_chain, device=dev)
-    lab = torch.empty((4 * 2 * n_chain, 24), dtype=torch.uint8, device=dev)
+        slot_label[:, j] = 8 * torch.arange(n_chain, device=dev) + 4 * rep + order.index(slot.subtask)
     alive = torch.empty(len(plan), dtype=torch.int64, device=dev)
     ms = []
     for k in range(reps + 1):
@@ -736,10 +740,8 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for si, (g, ws) in enumerate(graphs):
-            g.replay()
-            lab[2 * n_chain * si:2 * n_chain * (si + 1)].copy_(ws.labels)
-        L.check(L.lib().tl_chain_progress(L.ptr(lab), L.ptr(slot_label), n_chain, len(plan),
+        g.replay()
+        L.check(L.lib().tl_chain_progress(L.ptr(ws.labels), L.ptr(slot_label), n_chain, len(plan),
                                           L.ptr(alive), L.stream_ptr()), "chain")
         if world > 1:
             torch.distributed.all_reduce(alive)
@@ -750,8 +752,8 @@ def c4_run(dev, stream, world, flush=None, n_chain=4096, reps=5):
     t = max_over_ranks([sum(ms) / len(ms)], world, dev)[0] / 1e3
     curve = [100.0 * int(x) / (n_chain * world) for x in alive.cpu().tolist()]
     return {"workload": "C4: SetTable chains (settable plan, 16 slots), 4096 chains/GPU, "
-                        "8 fuzz episodes per chain (seeds 8c+k), one fused fuzz graph per "
-                        "subtask, progressive_completion",
+                        "8 fuzz episodes per chain (seeds 8c+k), one fused mixed-subtask fuzz "
+                        "graph, progressive_completion",
             "chains_per_gpu": n_chain, "n_gpus": world, "ms": 1e3 * t,
             "chains_per_s": n_chain * world / t,
             "labelled_trajectories_per_s": 8 * n_chain * world / t,

@@ -272,6 +272,28 @@ int tl_fuzz_ev(const int64_t* seeds, int32_t n_env, int32_t subtask,
                tl_label* labels, int64_t* ev_off, uint8_t* ev_kind, int32_t* ev_t,
                int64_t ev_capacity, void* scratch, void* stream);
 
+/* tl_fuzz / tl_fuzz_ev with a subtask per episode (subtasks[n_env] u8,
+ * device: 0 Pick, 1 Place, 2 Open, 3 Close), one launch sequence for a
+ * mixed batch -- e.g. the SetTable chains of C4 (Open, Pick, Place, Close
+ * episodes of every chain).  Episode e is fuzz(seeds[e], subtasks[e]); an
+ * out-of-range subtask gives that episode status TL_E_INVALID and no
+ * records.  The other arguments as for tl_fuzz / tl_fuzz_ev.              */
+int tl_fuzz_mixed(const int64_t* seeds, const uint8_t* subtasks, int32_t n_env,
+                  const tl_fuzz_cfg* cfg /* host */,
+                  const tl_thresholds* th_realize /* host */,
+                  const tl_cset* label_csets, const tl_rules* rules /* host */,
+                  tl_records* out, int32_t cap_per_env, uint8_t* script_kind,
+                  int32_t* script_gap, tl_script* scripts, uint8_t* step_mask,
+                  tl_label* labels, void* scratch, void* stream);
+int tl_fuzz_ev_mixed(const int64_t* seeds, const uint8_t* subtasks, int32_t n_env,
+                     const tl_fuzz_cfg* cfg /* host */,
+                     const tl_thresholds* th_realize /* host */,
+                     const tl_cset* label_csets, const tl_rules* rules /* host */,
+                     tl_records* out, int32_t cap_per_env, uint8_t* script_kind,
+                     int32_t* script_gap, tl_script* scripts, uint8_t* step_mask,
+                     tl_label* labels, int64_t* ev_off, uint8_t* ev_kind, int32_t* ev_t,
+                     int64_t ev_capacity, void* scratch, void* stream);
+
 /* realize given scripts (device array) then label; out->rec_start/n_rec
  * are INPUTS here (host computed the layout).  label_csets indexed
  * [subtask*3 + articulation kind]; episodes may mix subtasks.

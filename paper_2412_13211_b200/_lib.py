@@ -160,6 +160,11 @@ def lib():
         "tl_fuzz_ev": ([vp, i32, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
                         P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
                        ctypes.c_int),
+        "tl_fuzz_mixed": ([vp, vp, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
+                           P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "tl_fuzz_ev_mixed": ([vp, vp, i32, P(FuzzCfg_c), P(Thresholds_c), vp, vp,
+                              P(Records_c), i32, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
+                             ctypes.c_int),
         "tl_realize_scratch_bytes": ([i32], ctypes.c_size_t),
         "tl_realize": ([vp, vp, vp, i32, P(Thresholds_c), vp, vp, P(Records_c),
                         vp, vp, vp, vp], ctypes.c_int),
@@ -206,6 +211,7 @@ def exported_symbols():
             "tl_scan_emit_events", "tl_env_state_bytes", "tl_env_reset",
             "tl_env_reset_fuzz", "tl_env_step", "tl_env_labels", "tl_env_script_actions",
             "tl_group_mode_counts", "tl_chain_progress", "tl_filter_buckets", "tl_fuzz_ev",
+            "tl_fuzz_mixed", "tl_fuzz_ev_mixed",
             "tl_allgather_labels", "tl_allreduce_counts", "tl_validate_records"]
 
 

@@ -472,17 +472,25 @@ class SynthWorkspace:
         return RecordBatch(self.planes, self.grasped, self.rec_start, self.n_rec, self.dof)
 
 
-def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
+def fuzz_batch(seeds, subtask, cfg, th_realize: Thresholds, label_csets,
                ws: Optional[SynthWorkspace] = None, want_scripts=False,
                rules=None, events=False) -> SynthBatch:
     """tl_fuzz: fuzz(seed) -> records + labels for every seed (one launch).
     events=True: tl_fuzz_ev, the ordered event lists built inside the same
-    launch (SynthBatch.label_result holds ev_off / ev_kind / ev_t)."""
+    launch (SynthBatch.label_result holds ev_off / ev_kind / ev_t).
+    subtask: one subtask index for the batch, or one per seed (array /
+    tensor: tl_fuzz_mixed / tl_fuzz_ev_mixed)."""
     torch = _torch()
     dev = L.device()
     if not torch.is_tensor(seeds):
         seeds = torch.as_tensor(np.asarray(seeds, np.int64), device=dev)
     n = int(seeds.shape[0])
+    mixed = torch.is_tensor(subtask) or isinstance(subtask, (list, tuple, np.ndarray))
+    if mixed:
+        subs = torch.as_tensor(np.asarray(subtask.cpu() if torch.is_tensor(subtask) else subtask),
+                               dtype=torch.uint8).to(dev)
+        if int(subs.shape[0]) != n:
+            raise ValueError(f"{int(subs.shape[0])} subtasks for {n} seeds")
     cap = fuzz_capacity(cfg)
     if (ws is None or ws.n_env < n or ws.cap != cap or ws.max_steps != cfg.max_events + 4
             or (want_scripts and ws.scripts is None)):
@@ -491,7 +499,8 @@ def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
     c_cfg = L.FuzzCfg_c(cfg.max_events, cfg.max_gap, cfg.max_tail, 0,
                         float(cfg.edge_density), float(cfg.success_prob))
     rc_rules = rules_c(rules)
-    args = [L.ptr(seeds), n, int(subtask), ctypes.byref(c_cfg),
+    args = [L.ptr(seeds), *((L.ptr(subs),) if mixed else ()), n,
+            *(() if mixed else (int(subtask),)), ctypes.byref(c_cfg),
             ctypes.byref(thresholds_c(th_realize)), L.ptr(label_csets),
             ctypes.byref(rc_rules) if rc_rules is not None else None,
             ctypes.byref(rb.c()), cap,
@@ -505,13 +514,15 @@ def fuzz_batch(seeds, subtask: int, cfg, th_realize: Thresholds, label_csets,
         ev_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
         ev_kind = torch.empty(ev_cap, dtype=torch.uint8, device=dev)
         ev_t = torch.empty(ev_cap, dtype=torch.int32, device=dev)
-        rc = L.lib().tl_fuzz_ev(*args, L.ptr(ev_off), L.ptr(ev_kind), L.ptr(ev_t), ev_cap,
-                                L.ptr(ws.scratch), L.stream_ptr())
+        fn = L.lib().tl_fuzz_ev_mixed if mixed else L.lib().tl_fuzz_ev
+        rc = fn(*args, L.ptr(ev_off), L.ptr(ev_kind), L.ptr(ev_t), ev_cap,
+                L.ptr(ws.scratch), L.stream_ptr())
         L.check(rc, "tl_fuzz_ev")
         res = LabelResult(ws.labels, ws.step_mask, None)
         res.ev_off, res.ev_kind, res.ev_t = ev_off, ev_kind, ev_t
     else:
-        rc = L.lib().tl_fuzz(*args, L.ptr(ws.scratch), L.stream_ptr())
+        fn = L.lib().tl_fuzz_mixed if mixed else L.lib().tl_fuzz
+        rc = fn(*args, L.ptr(ws.scratch), L.stream_ptr())
         L.check(rc, "tl_fuzz")
     return SynthBatch(rb, ws.labels, ws.step_mask,
                       ws.scripts if want_scripts else None,

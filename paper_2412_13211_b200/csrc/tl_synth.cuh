@@ -44,6 +44,7 @@ struct SynthParams {
   // fuzz inputs (k_fuzz_reset)
   const int64_t* seeds;
   int32_t fuzz_subtask;
+  const uint8_t* subtasks;  // per-episode subtask (tl_fuzz*_mixed), else fuzz_subtask
   tl_fuzz_cfg cfg;
   // scripts (written by k_fuzz_reset, or given for realize)
   tl_script* scripts;
@@ -420,15 +421,23 @@ __device__ __forceinline__ int reset_script(const SynthParams& p, int64_t e, int
   uint8_t* sk = p.step_kind + e * ms;
   int32_t* sg = p.step_gap + e * ms;
   // at most max_events + 4 = ms steps are ever produced (synth.py:463-505)
-  int64_t gaps;
-  const int ns = sample_script(R, p.fuzz_subtask, p.cfg, sk, sg, t, ms, gaps);
-  int64_t nr = 1 + (ns < 0 ? 0 : gaps);
-  const int64_t tmin = ns > 0 ? 0 : 1;
-  nr += t.tail > tmin ? t.tail : tmin;
-  if (nr < 2) nr = 2;
+  int64_t gaps = 0;
+  const int sub = p.subtasks ? (int)p.subtasks[e] : p.fuzz_subtask;
+  int ns = -1;
+  int64_t nr = 2;
+  if (sub >= 0 && sub <= 3) {
+    ns = sample_script(R, sub, p.cfg, sk, sg, t, ms, gaps);
+    nr = 1 + (ns < 0 ? 0 : gaps);
+    const int64_t tmin = ns > 0 ? 0 : 1;
+    nr += t.tail > tmin ? t.tail : tmin;
+    if (nr < 2) nr = 2;
+  } else {
+    memset(&t, 0, sizeof(t));
+  }
   t.step_off = e * ms;
   t.seed = seed ^ 0x5EED;
-  t.n_steps = (ns < 0 || nr > p.cap_per_env) ? -1 : ns;  // -1: capacity error
+  // -1: capacity error, -2: no such subtask (a per-episode TL_E_INVALID)
+  t.n_steps = (sub < 0 || sub > 3) ? -2 : (ns < 0 || nr > p.cap_per_env) ? -1 : ns;
   p.scripts[e] = t;
   // length bucket for the realize kernel's longest-first claims
   const int b = t.n_steps < 0 ? 0 : (int)min((int64_t)kLenBuckets - 1, (nr - 1) / kBucketRecs);

@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_synth_warp(SynthParams p) 
     if (FUZZ && sc.n_steps < 0) {
       if (lane == 0) {
         tl_label L;
-        L.status = TL_ERR_SCRIPT_CAPACITY; L.n_events = 0; L.err_index = -1;
+        L.status = sc.n_steps == -2 ? TL_E_INVALID : TL_ERR_SCRIPT_CAPACITY;
+        L.n_events = 0; L.err_index = -1;
         L.subtask = (uint8_t)sc.subtask; L.mode = 255; L.flags = 0; L.pad = 0;
         L.d0 = __longlong_as_double(0x7ff8000000000000ll);
         p.labels[e] = L;

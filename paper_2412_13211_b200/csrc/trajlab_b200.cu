@@ -474,14 +474,15 @@ size_t tl_realize_scratch_bytes(int32_t n_env) {
   return align256((size_t)(n_env > 0 ? n_env : 1) * kMtN * 4) + 256;  // states + tickets
 }
 
-static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_cfg* cfg,
+static int fuzz_impl(const int64_t* seeds, const uint8_t* subtasks, int32_t n_env, int32_t subtask,
+                     const tl_fuzz_cfg* cfg,
                      const tl_thresholds* th_realize, const tl_cset* label_csets,
                      const tl_rules* rules, tl_records* out, int32_t cap_per_env,
                      uint8_t* script_kind, int32_t* script_gap, tl_script* scripts,
                      uint8_t* step_mask, tl_label* labels, int64_t* ev_off, uint8_t* ev_kind,
                      int32_t* ev_t, void* scratch, void* stream) {
   if (!cfg || !th_realize || !label_csets || !out || !labels || !scratch || n_env < 0 ||
-      subtask < 0 || subtask > 3 || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
+      (!subtasks && (subtask < 0 || subtask > 3)) || out->dtype != 0 || out->dof < 1 || out->dof > TL_MAX_DOF ||
       cfg->max_gap < 1 || cfg->max_tail < 1 || cfg->max_events < 0 ||
       cap_per_env < 2 || (script_kind && !script_gap) ||
       (!script_kind && script_gap))
@@ -509,6 +510,7 @@ static int fuzz_impl(const int64_t* seeds, int32_t n_env, int32_t subtask, const
   if (cap_per_env <= 64) sp.order = nullptr;  // every episode fits one wave: index order
   sp.seeds = seeds;
   sp.fuzz_subtask = subtask;
+  sp.subtasks = subtasks;
   sp.cfg = *cfg;
   sp.n_env = n_env;
   sp.cap_per_env = cap_per_env;
@@ -535,7 +537,7 @@ int tl_fuzz(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fuzz_
             tl_records* out, int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
             tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* scratch,
             void* stream) {
-  return fuzz_impl(seeds, n_env, subtask, cfg, th_realize, label_csets, rules, out, cap_per_env,
+  return fuzz_impl(seeds, nullptr, n_env, subtask, cfg, th_realize, label_csets, rules, out, cap_per_env,
                    script_kind, script_gap, scripts, step_mask, labels, nullptr, nullptr, nullptr,
                    scratch, stream);
 }
@@ -550,9 +552,37 @@ int tl_fuzz_ev(const int64_t* seeds, int32_t n_env, int32_t subtask, const tl_fu
       ev_capacity < (int64_t)n_env * cap_per_env * 4)  // <= 4 events per record (Open/Close)
     return TL_E_INVALID;
   if (n_env == 0) return cudaMemsetAsync(ev_off, 0, 8, S(stream)) ? TL_E_CUDA : TL_OK;
-  return fuzz_impl(seeds, n_env, subtask, cfg, th_realize, label_csets, rules, out, cap_per_env,
+  return fuzz_impl(seeds, nullptr, n_env, subtask, cfg, th_realize, label_csets, rules, out, cap_per_env,
                    script_kind, script_gap, scripts, step_mask, labels, ev_off, ev_kind, ev_t,
                    scratch, stream);
+}
+
+int tl_fuzz_mixed(const int64_t* seeds, const uint8_t* subtasks, int32_t n_env,
+                  const tl_fuzz_cfg* cfg, const tl_thresholds* th_realize,
+                  const tl_cset* label_csets, const tl_rules* rules, tl_records* out,
+                  int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
+                  tl_script* scripts, uint8_t* step_mask, tl_label* labels, void* scratch,
+                  void* stream) {
+  if (!subtasks && n_env > 0) return TL_E_INVALID;
+  return fuzz_impl(seeds, subtasks, n_env, 0, cfg, th_realize, label_csets, rules, out,
+                   cap_per_env, script_kind, script_gap, scripts, step_mask, labels, nullptr,
+                   nullptr, nullptr, scratch, stream);
+}
+
+int tl_fuzz_ev_mixed(const int64_t* seeds, const uint8_t* subtasks, int32_t n_env,
+                     const tl_fuzz_cfg* cfg, const tl_thresholds* th_realize,
+                     const tl_cset* label_csets, const tl_rules* rules, tl_records* out,
+                     int32_t cap_per_env, uint8_t* script_kind, int32_t* script_gap,
+                     tl_script* scripts, uint8_t* step_mask, tl_label* labels, int64_t* ev_off,
+                     uint8_t* ev_kind, int32_t* ev_t, int64_t ev_capacity, void* scratch,
+                     void* stream) {
+  if ((!subtasks && n_env > 0) || !ev_off || !ev_kind || !ev_t || !step_mask ||
+      ev_capacity < (int64_t)n_env * cap_per_env * 4)
+    return TL_E_INVALID;
+  if (n_env == 0) return cudaMemsetAsync(ev_off, 0, 8, S(stream)) ? TL_E_CUDA : TL_OK;
+  return fuzz_impl(seeds, subtasks, n_env, 0, cfg, th_realize, label_csets, rules, out,
+                   cap_per_env, script_kind, script_gap, scripts, step_mask, labels, ev_off,
+                   ev_kind, ev_t, scratch, stream);
 }
 
 int tl_realize(const tl_script* scripts, const uint8_t* step_kind, const int32_t* step_gap,

@@ -622,3 +622,48 @@ def test_short_wave_multi_window_vs_oracle(C, TH, kind):
         p, _ = from_oracle_records(O, recs)
         assert same_bits_f32(planes[:, rs[i]:rs[i] + len(recs)], p), i
     assert multi > 10
+
+
+@pytest.mark.parametrize("long_cfg", [False, True])
+def test_fuzz_mixed_subtasks_match_per_subtask_batches(C, TH, long_cfg):
+    """tl_fuzz_ev_mixed (a subtask per episode: the C4 chain batch) == the
+    four single-subtask tl_fuzz_ev batches on the same seeds -- labels, record
+    counts, records and ordered event lists; an out-of-range subtask gives
+    that episode TL_E_INVALID and no records."""
+    from paper_2412_13211_b200 import _lib as L
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig(max_gap=64, max_tail=64) if long_cfg else FuzzConfig()
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 3000
+    rng = np.random.default_rng(11 + long_cfg)
+    seeds = rng.integers(0, 2**40, n).astype(np.int64)
+    subs = rng.integers(0, 4, n).astype(np.uint8)
+    subs[[5, 777, 2999]] = [4, 9, 255]
+    mixed = C.fuzz_batch(seeds, subs, cfg, TH(), cs, events=True)
+    m_lab = mixed.labels.cpu().numpy()
+    m_lv = m_lab.reshape(-1).view(L.LABEL_DTYPE)
+    m_nrec = mixed.records.n_rec.cpu().numpy()
+    m_rs = mixed.records.rec_start.cpu().numpy()
+    m_pl = mixed.records.planes.cpu().numpy()
+    m_off = mixed.label_result.ev_off.cpu().numpy()
+    m_k = mixed.label_result.ev_kind.cpu().numpy()
+    m_t = mixed.label_result.ev_t.cpu().numpy()
+    bad = subs > 3
+    assert np.all(m_lv["status"][bad] == 100) and np.all(m_nrec[bad] == 0)
+    assert np.all(m_off[1:][bad] == m_off[:-1][bad])
+    for k in range(4):
+        idx = np.nonzero(subs == k)[0]
+        one = C.fuzz_batch(seeds[idx], k, cfg, TH(), cs, events=True)
+        assert np.array_equal(one.labels.cpu().numpy(), m_lab[idx]), k
+        nrec = one.records.n_rec.cpu().numpy()
+        assert np.array_equal(nrec, m_nrec[idx]), k
+        rs = one.records.rec_start.cpu().numpy()
+        pl = one.records.planes.cpu().numpy()
+        off = one.label_result.ev_off.cpu().numpy()
+        ek = one.label_result.ev_kind.cpu().numpy()
+        et = one.label_result.ev_t.cpu().numpy()
+        for j, e in enumerate(idx):
+            assert same_bits_f32(pl[:, rs[j]:rs[j] + nrec[j]], m_pl[:, m_rs[e]:m_rs[e] + nrec[j]]), (k, e)
+            a, b = off[j], off[j + 1]
+            c, d = m_off[e], m_off[e + 1]
+            assert np.array_equal(ek[a:b], m_k[c:d]) and np.array_equal(et[a:b], m_t[c:d]), (k, e)
