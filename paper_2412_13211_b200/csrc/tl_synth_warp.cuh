@@ -63,27 +63,35 @@ __device__ __forceinline__ void twist_phase_warp(uint32_t* mt, uint32_t* ring, u
   constexpr int kPer = (G1 - G0 + 31) / 32;
   constexpr uint32_t kMask = WarpCfg<DOFMAX>::kMask;
   const int lane = lane_id();
+  const uint4* mt4 = reinterpret_cast<const uint4*>(mt);
   uint4 nv[kPer];
 #pragma unroll
   for (int q = 0; q < kPer; q++) {
     const int g = G0 + lane + 32 * q;
-    if (g < G1) {
-      const uint4 cur = reinterpret_cast<const uint4*>(mt)[g];
-      const int i = 4 * g;
-      uint32_t nxt;
+    const int gg = g < G1 ? g : G1 - 1;  // lanes past the phase load a valid group
+    const int i = 4 * gg;
+    const uint4 cur = mt4[gg];
+    // the group's four sources i+k+397 (i+k < 227) or i+k-227 sit one word
+    // past a 16-byte boundary: one 128-bit load + the next group's first
+    // word (two requests instead of four 4-way conflicted scalar loads);
+    // phase 2's first group takes 621..623 and word 0
+    int sb;
+    if constexpr (G1 * 4 <= kMtN - kMtM) sb = i + kMtM - 1;
+    else if constexpr (G0 * 4 >= kMtN - kMtM + 1) sb = i - (kMtN - kMtM) - 1;
+    else sb = i < kMtN - kMtM ? i + kMtM - 1 : i - (kMtN - kMtM) - 1;
+    const uint4 sa = mt4[sb >> 2];
+    const uint32_t s3 = mt[sb + 4 == kMtN ? 0 : sb + 4];
+    // word i+4 (old; new word 0 for the block's last group) = the next
+    // lane's first word, except at the end of the 32-group chunk
+    uint32_t nxt = __shfl_down_sync(kFull, cur.x, 1);
+    if (lane == 31 || g + 1 >= G1) {
       if constexpr (G1 * 4 == kMtN) nxt = mt[i + 4 == kMtN ? 0 : i + 4];
       else nxt = mt[i + 4];
-      auto src = [&](int k) {  // phases 1 and 3 lie wholly on one side of word 227
-        const int ii = i + k;
-        if constexpr (G1 * 4 <= kMtN - kMtM) return mt[ii + kMtM];
-        else if constexpr (G0 * 4 >= kMtN - kMtM) return mt[ii - (kMtN - kMtM)];
-        else return mt[ii < kMtN - kMtM ? ii + kMtM : ii - (kMtN - kMtM)];
-      };
-      nv[q].x = mt_mix(cur.x, cur.y, src(0));
-      nv[q].y = mt_mix(cur.y, cur.z, src(1));
-      nv[q].z = mt_mix(cur.z, cur.w, src(2));
-      nv[q].w = mt_mix(cur.w, nxt, src(3));
     }
+    nv[q].x = mt_mix(cur.x, cur.y, sa.y);
+    nv[q].y = mt_mix(cur.y, cur.z, sa.z);
+    nv[q].z = mt_mix(cur.z, cur.w, sa.w);
+    nv[q].w = mt_mix(cur.w, nxt, s3);
   }
   __syncwarp();
 #pragma unroll
