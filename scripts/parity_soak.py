@@ -29,7 +29,8 @@ CHUNK = 8192
 REC_SAMPLE = 4096
 cs = core.synth_csets(Thresholds()).to_device(torch.device("cuda"))
 threads = os.cpu_count() or 1
-out = {"threads": threads, "configs": []}
+L.lib()
+out = {"threads": threads, "library": os.path.basename(L.LIB_PATH), "configs": []}
 t_start = time.time()
 for name, kw, n_total, seed_base in (("default", {}, n_def, 7_000_000),
                                      ("headline", {"max_gap": 64, "max_tail": 64}, n_long, 9_000_000)):
