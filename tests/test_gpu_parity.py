@@ -667,3 +667,31 @@ def test_fuzz_mixed_subtasks_match_per_subtask_batches(C, TH, long_cfg):
             a, b = off[j], off[j + 1]
             c, d = m_off[e], m_off[e + 1]
             assert np.array_equal(ek[a:b], m_k[c:d]) and np.array_equal(et[a:b], m_t[c:d]), (k, e)
+
+
+def test_fuzz_mixed_without_event_lists(C, TH):
+    """tl_fuzz_mixed (records + labels, no event lists) == per-subtask tl_fuzz."""
+    from paper_2412_13211_b200.synth import FuzzConfig
+    cfg = FuzzConfig()
+    cs = C.synth_csets(TH()).to_device(torch.device("cuda"))
+    n = 1500
+    seeds = np.arange(n, dtype=np.int64) * 7 + 123
+    subs = (np.arange(n) % 4).astype(np.uint8)[::-1].copy()
+    mixed = C.fuzz_batch(seeds, torch.from_numpy(subs), cfg, TH(), cs)
+    m_lab = mixed.labels.cpu().numpy()
+    m_nrec = mixed.records.n_rec.cpu().numpy()
+    m_rs = mixed.records.rec_start.cpu().numpy()
+    m_pl = mixed.records.planes.cpu().numpy()
+    m_mask = mixed.step_mask.cpu().numpy()
+    for k in range(4):
+        idx = np.nonzero(subs == k)[0]
+        one = C.fuzz_batch(seeds[idx], k, cfg, TH(), cs)
+        assert np.array_equal(one.labels.cpu().numpy(), m_lab[idx])
+        nrec = one.records.n_rec.cpu().numpy()
+        assert np.array_equal(nrec, m_nrec[idx])
+        rs = one.records.rec_start.cpu().numpy()
+        pl = one.records.planes.cpu().numpy()
+        mask = one.step_mask.cpu().numpy()
+        for j, e in enumerate(idx):
+            assert same_bits_f32(pl[:, rs[j]:rs[j] + nrec[j]], m_pl[:, m_rs[e]:m_rs[e] + nrec[j]])
+            assert np.array_equal(mask[rs[j]:rs[j] + nrec[j]], m_mask[m_rs[e]:m_rs[e] + nrec[j]])
